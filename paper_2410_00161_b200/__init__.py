@@ -1,0 +1,57 @@
+"""B200-native KV-Compress hot path: variable-head-rate paged KV on sm_100a.
+
+Drop-in for the reference ``pagedkv`` package's hot path (cache config,
+block allocator, per-head block tables, metric update, eviction scheduling,
+cache moves, paged decode attention); see DESIGN.md.  The compute runs in
+libkvc.so (hand-written CUDA, C ABI in include/kvc.h); there is no CPU
+fallback.
+"""
+
+from .attention import AttentionConfig, paged_attention, paged_decode
+from .block_manager import BlockManager, blocks_needed_prefill
+from .budget import budget_to_blocks, per_sequence_budget
+from .cache import (
+    BlockTables,
+    SlotHandle,
+    UnifiedKVCache,
+    append_kv,
+    fragmentation,
+    lookup_kv,
+)
+from .compression import (
+    CompressionSchedule,
+    EvictionPlan,
+    compress,
+    execute_cache_moves,
+    schedule_evictions,
+)
+from .metrics import MetricConfig, MetricsStore, accumulate_decode
+from .prefill import prefill_sequence, window_metrics
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AttentionConfig",
+    "BlockManager",
+    "BlockTables",
+    "CompressionSchedule",
+    "EvictionPlan",
+    "MetricConfig",
+    "MetricsStore",
+    "SlotHandle",
+    "UnifiedKVCache",
+    "accumulate_decode",
+    "append_kv",
+    "blocks_needed_prefill",
+    "budget_to_blocks",
+    "compress",
+    "execute_cache_moves",
+    "fragmentation",
+    "lookup_kv",
+    "paged_attention",
+    "paged_decode",
+    "per_sequence_budget",
+    "prefill_sequence",
+    "schedule_evictions",
+    "window_metrics",
+]

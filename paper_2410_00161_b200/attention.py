@@ -1,0 +1,121 @@
+"""Paged GQA decode attention over ragged per-KV-head tables (K1).
+
+Drop-in for pagedkv.attention.paged_attention (attention.py:92-127) plus the
+batched, fused engine path ``paged_decode``: one launch per layer appends the
+step's K/V, attends every (sequence, KV head) of the batch and folds the
+attention mass into the eviction metrics (engine.py:426-444,
+metrics.py:189-211).  Both run the same sm_100a kernel (csrc/decode.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cache import BlockTables, UnifiedKVCache, pool_struct
+from .errors import NumericError
+
+
+@dataclass(frozen=True)
+class AttentionConfig:
+    num_query_heads: int
+    num_kv_heads: int
+    head_dim: int
+    num_layers: int
+
+    def __post_init__(self):
+        if self.num_query_heads % self.num_kv_heads != 0:
+            raise ValueError("num_query_heads must be divisible by num_kv_heads")
+
+    @property
+    def group_size(self) -> int:
+        return self.num_query_heads // self.num_kv_heads
+
+
+def _bf16(x, dev) -> torch.Tensor:
+    if not torch.is_tensor(x):
+        x = torch.as_tensor(np.asarray(x))
+    return x.to(dev, torch.bfloat16).contiguous()
+
+
+def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables, seq_ids,
+                 layer: int, cfg: AttentionConfig, store=None, metric_mode: int = 0,
+                 k_new: torch.Tensor | None = None, v_new: torch.Tensor | None = None,
+                 fresh: bool = True, out: torch.Tensor | None = None, out_f32: bool = False,
+                 rows_out: torch.Tensor | None = None, rows_tensor: torch.Tensor | None = None,
+                 host_rows: list | None = None, max_ctx: int | None = None,
+                 splits: int = 0) -> torch.Tensor:
+    """Batched single-token decode for one layer (asynchronous, no host sync).
+
+    query (B, n_q, d) bf16; k_new/v_new (B, H, d) bf16 are appended at each
+    head's position C before attending (their blocks must already exist);
+    metric_mode 1/2 adds sum_h p (L1) or p^2 (L2) to every attended slot's
+    metric.  rows_out, if given, receives the (B, H, r, stride) weights.
+    Returns out (B, n_q, d) bf16 (f32 with out_f32).
+    """
+    dev = cache.device
+    B = query.shape[0]
+    if host_rows is None:
+        host_rows = [tables.row(s) for s in seq_ids]
+    if rows_tensor is None:
+        rows_tensor = torch.tensor(host_rows, dtype=torch.int32, device=dev)
+    if out is None:
+        out = torch.empty((B, cfg.num_query_heads, cfg.head_dim),
+                          dtype=torch.float32 if out_f32 else torch.bfloat16, device=dev)
+    append = k_new is not None
+    if max_ctx is None:
+        max_ctx = max((tables.ctx_bound[r] for r in host_rows), default=1)
+        max_ctx += 1 if append else 0
+    if append:
+        for r in host_rows:
+            tables.ctx_bound[r] += 1
+    a = _lib.DecodeArgs()
+    a.seq_rows = rows_tensor.data_ptr()
+    a.batch = B
+    a.layer = layer
+    a.num_query_heads = cfg.num_query_heads
+    a.q = query.data_ptr()
+    a.k_new = _lib.ptr(k_new)
+    a.v_new = _lib.ptr(v_new)
+    a.out = out.data_ptr()
+    a.out_f32 = int(out.dtype == torch.float32)
+    a.rows_out = _lib.ptr(rows_out)
+    a.rows_stride = rows_out.shape[-1] if rows_out is not None else 0
+    a.metric_mode = metric_mode
+    a.append_fresh = int(fresh)
+    a.max_ctx = max(1, int(max_ctx))
+    a.splits = splits
+    p = pool_struct(cache=cache, tables=tables, store=store)
+    _lib.check(_lib.lib().kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)),
+               "paged_decode")
+    return out
+
+
+def paged_attention(query, cache: UnifiedKVCache, tables: BlockTables, seq_id: int, layer: int,
+                    cfg: AttentionConfig):
+    """Single-token decode attention over the paged (possibly compressed) cache.
+
+    ``query`` is (num_query_heads, head_dim).  Each query head gathers the
+    live KVs of its KV head through the block table, in slot order 0..C-1.
+    Returns the (num_query_heads, head_dim) fp32 output plus, per KV head,
+    the (group_size, C) attention weights (attention.py:92-127).
+    """
+    dev = cache.device
+    qt = query if torch.is_tensor(query) else torch.as_tensor(np.asarray(query))
+    if not torch.isfinite(qt).all():
+        raise NumericError("non-finite values in attention inputs")
+    q = _bf16(qt, dev).reshape(1, cfg.num_query_heads, cfg.head_dim)
+    row = tables.row(seq_id)
+    ctx = tables.ctx[row, layer].tolist()
+    cmax = max(max(ctx), 1)
+    r = cfg.group_size
+    rows = torch.zeros((1, cfg.num_kv_heads, r, cmax), dtype=torch.float32, device=dev)
+    rt = torch.tensor([row], dtype=torch.int32, device=dev)
+    out = paged_decode(q, cache, tables, None, layer, cfg, out_f32=True, rows_out=rows,
+                       rows_tensor=rt, host_rows=[row], max_ctx=cmax)
+    _lib.DeviceContext.get(dev).raise_status()
+    return out[0], [rows[0, h, :, : ctx[h]] for h in range(cfg.num_kv_heads)]

@@ -1,0 +1,38 @@
+"""__graft_entry__.smoke(): one small decode step on cuda:0 checked against
+the CPU oracle (the oracle is only the checker)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def run_smoke():
+    from gpu_rig import DevRig, bf16_round, random_state
+    from oracle import kvc_oracle as O
+    import paper_2410_00161_b200 as K
+    from paper_2410_00161_b200 import _lib
+
+    assert torch.cuda.is_available(), "smoke needs cuda:0"
+    rng = np.random.default_rng(0)
+    b, d, heads, r, layers = 16, 128, 4, 4, 1
+    seqs = [0, 1]
+    st = random_state(rng, 2048, b, d, layers, heads, seqs, 400)
+    rig = DevRig(2048, b, d, layers, heads)
+    rig.load(st)
+    cfg = K.AttentionConfig(heads * r, heads, d, layers)
+    assert rig.manager.allocate_decode_step(seqs) == O.alloc_decode(st, seqs)
+    q = bf16_round(rng.standard_normal((2, heads * r, d)))
+    kn = bf16_round(rng.standard_normal((2, heads, d)))
+    vn = bf16_round(rng.standard_normal((2, heads, d)))
+    t = lambda x: torch.from_numpy(x).to("cuda", torch.bfloat16)
+    out = K.paged_decode(t(q), rig.cache, rig.tables, seqs, 0, cfg, store=rig.store, metric_mode=2,
+                         k_new=t(kn), v_new=t(vn), out_f32=True)
+    _lib.DeviceContext.get(rig.cache.device).raise_status()
+    for i, s in enumerate(seqs):
+        ref, _ = O.decode_step_layer(st, s, 0, q[i], kn[i], vn[i], "L2")
+        err = float(np.abs(out[i].cpu().numpy() - ref).max())
+        assert err < 2e-3, err
+    dst = rig.to_oracle()
+    assert np.allclose(dst.metric, st.metric, rtol=1e-3, atol=1e-6)
+    print("smoke: decode parity ok")
