@@ -31,6 +31,7 @@
  *                                                             metrics.py:68-89,160-175
  *   kvc_schedule_evictions  build_views .. eviction_mask      compression.py:122-231
  *   kvc_execute_moves       move_cache + free_schedule_blocks compression.py:234-309
+ *   kvc_compress            compress (both of the above)      compression.py:312-355
  *   kvc_clear_fresh         MetricsStore.clear_fresh          metrics.py:185-186
  */
 #ifndef KVC_H_
@@ -228,6 +229,10 @@ int kvc_schedule_evictions(const kvc_pool *pool, const kvc_evict_args *args, voi
 /* Compaction + trailing free + logical renumbering using the counts the
  * previous kvc_schedule_evictions call left in args->evict. */
 int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *args, void *stream);
+
+/* schedule_evictions + execute_moves in one pass over the slots (the
+ * reference's compress, compression.py:312-355). */
+int kvc_compress(const kvc_pool *pool, const kvc_evict_args *args, void *stream);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,7 @@ _SIGS = {
     "kvc_window_metric": ([_p, _p, _p], _i32),
     "kvc_schedule_evictions": ([_p, _p, _p], _i32),
     "kvc_execute_moves": ([_p, _p, _p], _i32),
+    "kvc_compress": ([_p, _p, _p], _i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,0 +1,690 @@
+// K3 eviction scheduler + K4 compaction (MoveCache) for a batch of sequences.
+//
+// Reference (pkg/src/pagedkv/compression.py): per head, slots get an
+// effective metric (0 if empty, +inf if protected|fresh, :131-133) and are
+// sorted by (metric, occupied, logical, position) (:156-166); threshold
+// th[e-1] is the (b*e)-th smallest effective metric (:169-177); candidate
+// rows of a sequence are ranked by (threshold, head_idx, row) and the first
+// E rows with row < cap_h are evicted (:180-231); MoveCache then fills the
+// holes below each head's eviction range with the range's survivors
+// (:234-280) and the trailing blocks are freed and logicals renumbered
+// (:283-309).
+//
+// B200 formulation (no sort at all, exact):
+//  * #rows of head h with th <= v  ==  min(cap_h, floor(cnt_h(<= v) / b)),
+//    where cnt_h counts slots with key <= v.  So the E-th smallest eligible
+//    threshold T* of a sequence is found by an MSB radix search (11+11+10
+//    bits) over per-head histograms of 32-bit order keys, with per-head
+//    contributions min(cap, floor(cnt/b)) summed per sequence.
+//  * e_h = L_h + take_h with L_h/U_h = rows with th < / <= T*, ties taken
+//    in head order (head_idx is the reference's tie-break).
+//  * the evicted slot set of a head = keys < T_h plus the first `need` ties
+//    at T_h = (b*e_h)-th smallest key, ties ordered by (occupied, logical,
+//    position) - a per-head radix select, not a sort.
+//  * MoveCache pairing: k-th hole (ascending) below the range <-> k-th
+//    survivor (descending) inside it; all pairs are disjoint, so K/V/metric
+//    copies run concurrently.  Logical renumbering = rank via a bitmap
+//    prefix-popcount (logicals are distinct).
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+
+using namespace kvc;
+
+namespace {
+
+constexpr int kBins = 2048;       // 11-bit digits
+constexpr int kThreads = 512;
+constexpr uint32_t kKeyInf = 0xFF800000u;  // f32_order_key(+inf)
+
+struct EvictState {
+  // per head (T = n_seqs * hp)
+  uint32_t *keys;     // [T][max_slots]
+  int32_t *cap;       // [T]
+  int32_t *lo;        // [T] L_h
+  int32_t *hi;        // [T] U_h
+  // per sequence
+  int32_t *R;         // [n_seqs][kBins] contribution deltas per digit
+  uint32_t *prefix;   // [n_seqs] T* digits found so far
+  int64_t *E;         // [n_seqs] clamped budget (0 = inactive)
+  int64_t max_slots;
+  int hp;
+  int32_t *status;
+};
+
+__device__ __forceinline__ uint32_t slot_key(const kvc_pool &p, int64_t f, bool occ) {
+  if (!occ) return f32_order_key(0.f);
+  if (p.protected_[f] | p.fresh[f]) return kKeyInf;
+  return f32_order_key(p.metric[f]);
+}
+
+// Warp-aggregated shared-memory histogram increment.
+__device__ __forceinline__ void hist_add(int32_t *hist, uint32_t bin, bool active) {
+  const unsigned mask = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const unsigned peers = __match_any_sync(mask, bin);
+  const int leader = __ffs(peers) - 1;
+  if ((threadIdx.x & 31) == leader) atomicAdd(&hist[bin], __popc(peers));
+}
+
+// Per-head inclusive scan of a kBins histogram in smem (kThreads threads,
+// 4 bins each).  Writes the inclusive cumulative counts back into hist.
+__device__ void scan_hist(int32_t *hist) {
+  using Scan = cub::BlockScan<int32_t, kThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int per = kBins / kThreads;
+  int32_t v[per];
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    v[i] = hist[threadIdx.x * per + i];
+    s += v[i];
+  }
+  int32_t excl;
+  __syncthreads();
+  Scan(tmp).ExclusiveSum(s, excl);
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    excl += v[i];
+    hist[threadIdx.x * per + i] = excl;
+  }
+  __syncthreads();
+}
+
+// Add this head's contribution deltas min(cap, floor((base+cum[c])/b)) to R.
+__device__ void add_contrib(const int32_t *cum, int64_t base, int cap, int b, int32_t *R, int nbins) {
+  for (int c = threadIdx.x; c < nbins; c += kThreads) {
+    // delta form: bin 0 carries the absolute value, later bins the increase
+    int64_t z = (base + cum[c]) / b;
+    if (z > cap) z = cap;
+    int64_t a = 0;
+    if (c > 0) {
+      a = (base + cum[c - 1]) / b;
+      if (a > cap) a = cap;
+    }
+    if (z > a) atomicAdd(&R[c], (int32_t)(z - a));
+  }
+}
+
+// (1) keys + cap + level-1 histogram contributions.
+__global__ void __launch_bounds__(kThreads) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
+                                                  EvictState S, int with_hist) {
+  __shared__ int32_t hist[kBins];
+  __shared__ int32_t shield_s;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int b = p.block_size;
+  const int nb = p.nblocks[hidx];
+  const int C = p.ctx[hidx];
+  const int64_t n = (int64_t)nb * b;
+  const int32_t *tab = head_table(p, hidx);
+  uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+  if (n > S.max_slots) {
+    if (threadIdx.x == 0) set_status(p.status, KVC_DEV_CAPACITY, (int32_t)hidx, (int32_t)n);
+    return;
+  }
+  for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+  if (threadIdx.x == 0) shield_s = 0;
+  __syncthreads();
+  int shield = 0;
+  for (int64_t base = 0; base < n; base += kThreads) {
+    const int64_t pos = base + threadIdx.x;
+    const bool in = pos < n;
+    uint32_t key = 0;
+    if (in) {
+      const int64_t f = (int64_t)tab[pos / b] * b + pos % b;
+      const bool occ = pos < C;
+      key = slot_key(p, f, occ);
+      shield += (occ && (p.protected_[f] | p.fresh[f])) ? 1 : 0;
+      keys[pos] = key;
+    }
+    if (with_hist) hist_add(hist, key >> 21, in);
+  }
+  atomicAdd(&shield_s, shield);
+  __syncthreads();
+  const int sh_blocks = (shield_s + b - 1) / b;
+  int cap = nb - (sh_blocks > 1 ? sh_blocks : 1);
+  if (cap < 0) cap = 0;
+  if (threadIdx.x == 0) S.cap[g] = cap;
+  if (!with_hist || req[si] <= 0) return;
+  scan_hist(hist);
+  add_contrib(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
+}
+
+// (2/4/6) per sequence: clamp E, find the first digit whose cumulative row
+// count reaches E, append it to the prefix, reset R.
+__global__ void __launch_bounds__(1024) k_find(const int64_t *req, EvictState S, int level, int bits,
+                                              int64_t *clamped) {
+  using Scan = cub::BlockScan<int32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int found;
+  const int si = blockIdx.x;
+  int32_t *R = S.R + (int64_t)si * kBins;
+  const int nbins = 1 << bits;
+  if (level == 1) {
+    // level 1 also computes the clamp: R summed over all bins = sum cap
+    if (req[si] <= 0) {
+      if (threadIdx.x == 0) { S.E[si] = 0; clamped[si] = req[si]; }  // min(req, sum cap) = req
+      for (int c = threadIdx.x; c < kBins; c += 1024) R[c] = 0;
+      return;
+    }
+  } else if (S.E[si] <= 0) {
+    return;
+  }
+  constexpr int per = kBins / 1024;
+  int32_t v[per];
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    const int c = threadIdx.x * per + i;
+    v[i] = c < nbins ? R[c] : 0;
+    s += v[i];
+  }
+  int32_t excl, total;
+  Scan(tmp).ExclusiveSum(s, excl, total);
+  if (threadIdx.x == 0) found = kBins;
+  __syncthreads();
+  int64_t E;
+  if (level == 1) {
+    E = req[si] < total ? req[si] : total;  // min(requested, sum cap)
+  } else {
+    E = S.E[si];
+  }
+  if (E > 0) {
+    int32_t run = excl;
+#pragma unroll
+    for (int i = 0; i < per; ++i) {
+      run += v[i];
+      const int c = threadIdx.x * per + i;
+      if (c < nbins && run >= E) { atomicMin(&found, c); break; }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kBins; c += 1024) R[c] = 0;
+  if (threadIdx.x == 0 && E > 0 && found >= nbins) set_status(S.status, KVC_DEV_SCHEDULE_CORRUPTION, si, level);
+  if (threadIdx.x == 0) {
+    if (level == 1) {
+      S.E[si] = E;
+      clamped[si] = E;
+      S.prefix[si] = (uint32_t)found;
+    } else {
+      S.prefix[si] = (S.prefix[si] << bits) | (uint32_t)found;
+    }
+  }
+}
+
+// (3/5) per head: histogram of the next digit among keys matching the prefix.
+__global__ void __launch_bounds__(kThreads) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
+                                                  int shift, int bits) {
+  __shared__ int32_t hist[kBins];
+  __shared__ int64_t below_s;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  if (S.E[si] <= 0) return;
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int b = p.block_size;
+  const int64_t n = (int64_t)p.nblocks[hidx] * b;
+  const uint32_t pre = S.prefix[si];
+  const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+  const uint32_t dmask = (1u << bits) - 1;
+  for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+  if (threadIdx.x == 0) below_s = 0;
+  __syncthreads();
+  int32_t below = 0;
+  for (int64_t base = 0; base < n; base += kThreads) {
+    const int64_t pos = base + threadIdx.x;
+    uint32_t key = pos < n ? keys[pos] : 0xffffffffu;
+    const uint32_t top = key >> shift_hi;
+    const bool match = pos < n && top == pre;
+    below += (pos < n && top < pre) ? 1 : 0;
+    hist_add(hist, (key >> shift) & dmask, match);
+  }
+  atomicAdd((unsigned long long *)&below_s, (unsigned long long)below);
+  __syncthreads();
+  scan_hist(hist);
+  add_contrib(hist, below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
+}
+
+// (7) per head: rows with threshold < T* and <= T*.
+__global__ void __launch_bounds__(kThreads) k_bounds(kvc_pool p, const int32_t *rows, EvictState S) {
+  using Red = cub::BlockReduce<int32_t, kThreads>;
+  __shared__ typename Red::TempStorage tmp;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  if (S.E[si] <= 0) {
+    if (threadIdx.x == 0) { S.lo[g] = 0; S.hi[g] = 0; }
+    return;
+  }
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int b = p.block_size;
+  const int64_t n = (int64_t)p.nblocks[hidx] * b;
+  const uint32_t T = S.prefix[si];
+  const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+  int32_t lt = 0, le = 0;
+  for (int64_t pos = threadIdx.x; pos < n; pos += kThreads) {
+    const uint32_t k = keys[pos];
+    lt += k < T;
+    le += k <= T;
+  }
+  lt = Red(tmp).Sum(lt);
+  __syncthreads();
+  le = Red(tmp).Sum(le);
+  if (threadIdx.x == 0) {
+    const int cap = S.cap[g];
+    S.lo[g] = lt / b < cap ? lt / b : cap;
+    S.hi[g] = le / b < cap ? le / b : cap;
+  }
+}
+
+// (8) one CTA: per sequence e_h = L_h + ties taken in head order; global
+// exclusive offsets of e_h*b for the move lists.
+__global__ void __launch_bounds__(1024) k_select(EvictState S, int n_seqs, int bsz, int32_t *evict,
+                                                int64_t *move_off, int32_t *status) {
+  using Scan = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t carry, less_s;
+  const int hp = S.hp;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int si = 0; si < n_seqs; ++si) {
+    const int64_t E = S.E[si];
+    // total rows strictly below T*
+    if (threadIdx.x == 0) less_s = 0;
+    __syncthreads();
+    int64_t less = 0;
+    for (int h = threadIdx.x; h < hp; h += 1024) less += E > 0 ? S.lo[(int64_t)si * hp + h] : 0;
+    atomicAdd((unsigned long long *)&less_s, (unsigned long long)less);
+    __syncthreads();
+    const int64_t need = E - less_s;  // tie rows to take at T*, in head order
+    int64_t tcarry = 0;
+    for (int base = 0; base < hp; base += 1024) {
+      const int h = base + threadIdx.x;
+      const int64_t g = (int64_t)si * hp + h;
+      int64_t ties = 0;
+      if (h < hp && E > 0) ties = S.hi[g] - S.lo[g];
+      int64_t excl, tot;
+      Scan(tmp).ExclusiveSum(ties, excl, tot);
+      if (h < hp) {
+        int64_t take = need - (tcarry + excl);
+        if (take < 0) take = 0;
+        if (take > ties) take = ties;
+        evict[g] = E > 0 ? (int32_t)(S.lo[g] + take) : 0;
+      }
+      __syncthreads();
+      tcarry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && E > 0 && (need < 0 || need > tcarry)) set_status(status, KVC_DEV_SCHEDULE_CORRUPTION, si, (int32_t)need);
+    __syncthreads();
+  }
+  // exclusive offsets over all heads of e_h * b (move capacity per head)
+  const int64_t T = (int64_t)n_seqs * hp;
+  for (int64_t base = 0; base < T; base += 1024) {
+    const int64_t g = base + threadIdx.x;
+    int64_t v = g < T ? (int64_t)evict[g] * bsz : 0;
+    int64_t excl, tot;
+    Scan(tmp).ExclusiveSum(v, excl, tot);
+    if (g < T) move_off[g] = carry + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) move_off[T] = carry;
+}
+
+// Radix select inside one CTA: value of the `rank`-th (0-based) smallest of
+// the values v(pos) over pos in [0, n) with pred(pos); returns the value and
+// leaves in *rank_out the rank of the target among values equal to it.
+template <typename GetV>
+__device__ uint32_t cta_select(int32_t *hist, int64_t n, int64_t rank, GetV getv, int64_t *rank_out) {
+  __shared__ uint32_t pre_s;
+  __shared__ int64_t rank_s;
+  const int shifts[3] = {21, 10, 0};
+  const int bitsv[3] = {11, 11, 10};
+  uint32_t pre = 0;
+  for (int lv = 0; lv < 3; ++lv) {
+    const int shift = shifts[lv], bits = bitsv[lv];
+    const int shift_hi = shift + bits;
+    const uint32_t dmask = (1u << bits) - 1;
+    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += kThreads) {
+      const int64_t pos = base + threadIdx.x;
+      bool ok = false;
+      uint32_t v = 0;
+      if (pos < n) ok = getv(pos, v);
+      const bool match = ok && (shift_hi >= 32 || (v >> shift_hi) == pre);
+      hist_add(hist, (v >> shift) & dmask, match);
+    }
+    __syncthreads();
+    scan_hist(hist);  // inclusive
+    for (int c = threadIdx.x; c < (1 << bits); c += kThreads) {
+      const int64_t excl = c > 0 ? hist[c - 1] : 0;
+      if (excl <= rank && rank < hist[c]) {
+        pre_s = (pre << bits) | (uint32_t)c;
+        rank_s = rank - excl;
+      }
+    }
+    __syncthreads();
+    pre = pre_s;
+    rank = rank_s;
+    __syncthreads();
+  }
+  *rank_out = rank;
+  return pre;
+}
+
+struct MoveArgs {
+  int32_t *evict;
+  int32_t *evicted_kvs;
+  int32_t *freed;       // nullable [T][max_blocks]
+  int32_t *moves;       // [cap][2]
+  int64_t *move_off;
+  int32_t *move_counts;
+  int64_t *totals;
+};
+
+// (9) per head with e > 0: mask, MoveCache pairing, copies, free, renumber.
+__global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t *rows, EvictState S,
+                                                     MoveArgs M) {
+  extern __shared__ uint32_t bitmap[];  // max_slots bits
+  __shared__ int32_t hist[kBins];
+  __shared__ int32_t cnt_s[4];
+  using Scan = cub::BlockScan<int32_t, kThreads>;
+  __shared__ typename Scan::TempStorage stmp;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  const int e = M.evict[g];
+  if (threadIdx.x == 0 && M.move_counts) M.move_counts[g] = 0;
+  if (threadIdx.x == 0 && M.evicted_kvs) M.evicted_kvs[g] = 0;
+  if (e <= 0) return;
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int b = p.block_size;
+  const int D = p.head_dim;
+  const int nb = p.nblocks[hidx];
+  const int C = p.ctx[hidx];
+  const int64_t n = (int64_t)nb * b;
+  int32_t *tab = head_table(p, hidx);
+  const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+  auto flat = [&](int64_t pos) { return (int64_t)tab[pos / b] * b + pos % b; };
+
+  // threshold T_h = (b*e)-th smallest key, then the tie cut S_h
+  int64_t tie_rank;
+  const int64_t target = (int64_t)b * e - 1;
+  const uint32_t T = cta_select(hist, n, target, [&](int64_t pos, uint32_t &v) { v = keys[pos]; return true; },
+                                &tie_rank);
+  auto sec = [&](int64_t pos) -> uint32_t {
+    const bool occ = pos < C;
+    return occ ? (0x80000000u | (uint32_t)(p.logical[flat(pos)] + 1)) : (uint32_t)pos;
+  };
+  int64_t dummy;
+  const uint32_t Sx = cta_select(hist, n, tie_rank, [&](int64_t pos, uint32_t &v) {
+    if (keys[pos] != T) return false;
+    v = sec(pos);
+    return true;
+  }, &dummy);
+  auto masked = [&](int64_t pos) {
+    const uint32_t k = keys[pos];
+    return k < T || (k == T && sec(pos) <= Sx);
+  };
+
+  // pairing: holes below R0 ascending -> dst; survivors in [R0, n) descending -> src
+  const int64_t R0 = n - (int64_t)e * b;
+  const int64_t off = M.move_off[g];
+  int32_t *mv = M.moves + off * 2;
+  if (threadIdx.x == 0) { cnt_s[0] = 0; cnt_s[1] = 0; cnt_s[2] = 0; }
+  __syncthreads();
+  int32_t evk = 0;
+  {
+    int32_t carry = 0;
+    for (int64_t base = 0; base < R0; base += kThreads) {
+      const int64_t pos = base + threadIdx.x;
+      int32_t hole = 0;
+      if (pos < R0) {
+        const bool m = masked(pos);
+        evk += (m && pos < C) ? 1 : 0;
+        hole = (m || p.logical[flat(pos)] < 0) ? 1 : 0;
+      }
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(hole, excl, tot);
+      if (hole) {
+        const int64_t k = carry + excl;
+        if (k < (int64_t)e * b) mv[2 * k + 1] = (int32_t)flat(pos);
+      }
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt_s[0] = carry;  // holes available
+  }
+  {
+    int32_t carry = 0;
+    for (int64_t base = 0; base < n - R0; base += kThreads) {
+      const int64_t pos = n - 1 - (base + threadIdx.x);  // descending
+      int32_t surv = 0;
+      if (pos >= R0) {
+        const bool m = masked(pos);
+        evk += (m && pos < C) ? 1 : 0;
+        surv = (!m && p.logical[flat(pos)] >= 0) ? 1 : 0;
+      }
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(surv, excl, tot);
+      if (surv) mv[2 * (carry + excl)] = (int32_t)flat(pos);
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt_s[1] = carry;  // survivors to move
+  }
+  atomicAdd(&cnt_s[2], evk);
+  __syncthreads();
+  const int32_t nmoves = cnt_s[1];
+  if (nmoves > cnt_s[0]) {
+    if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
+    return;
+  }
+  // concurrent moves: small fields per thread, K/V rows per warp (16 B lanes)
+  for (int k = threadIdx.x; k < nmoves; k += kThreads) {
+    const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
+    p.metric[dst] = p.metric[src];
+    p.logical[dst] = p.logical[src];
+    p.protected_[dst] = p.protected_[src];
+    p.fresh[dst] = p.fresh[src];
+  }
+  if (D % 8 != 0) {  // small head_dim: element copies
+    uint16_t *kc = reinterpret_cast<uint16_t *>(p.k_cache);
+    uint16_t *vc = reinterpret_cast<uint16_t *>(p.v_cache);
+    const int64_t total = (int64_t)nmoves * D;
+    for (int64_t i = threadIdx.x; i < total; i += kThreads) {
+      const int64_t k = i / D, c = i % D;
+      const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
+      kc[dst * D + c] = kc[src * D + c];
+      vc[dst * D + c] = vc[src * D + c];
+    }
+  } else {
+    const int vec = D / 8;  // 16-byte chunks per row
+    uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
+    uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
+    const int64_t total = (int64_t)nmoves * vec;
+    for (int64_t i = threadIdx.x; i < total; i += kThreads) {
+      const int64_t k = i / vec, c = i % vec;
+      const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
+      const uint4 kv = kc[src * vec + c];
+      const uint4 vv = vc[src * vec + c];
+      kc[dst * vec + c] = kv;
+      vc[dst * vec + c] = vv;
+    }
+  }
+  __syncthreads();
+  // free the trailing e blocks, reset their slots
+  for (int64_t i = threadIdx.x; i < (int64_t)e * b; i += kThreads) {
+    const int j = nb - e + (int)(i / b);
+    const int32_t blk = tab[j];
+    const int64_t f = (int64_t)blk * b + i % b;
+    p.metric[f] = 0.f;
+    p.logical[f] = -1;
+    p.protected_[f] = 0;
+    p.fresh[f] = 0;
+    if (i % b == 0) {
+      p.free_flag[blk] = 1;
+      atomicAdd(&p.free_tile[blk / KVC_FREE_TILE], 1);
+      if (M.freed) M.freed[(int64_t)g * p.max_blocks + (j - (nb - e))] = blk;
+    }
+  }
+  const int keep = nb - e;
+  const int Cn = C < keep * b ? C : keep * b;
+  // logical renumbering: rank among kept logicals (distinct, < n)
+  const int words = (int)((n + 31) / 32);
+  for (int w = threadIdx.x; w < words; w += kThreads) bitmap[w] = 0;
+  __syncthreads();
+  for (int64_t pos = threadIdx.x; pos < Cn; pos += kThreads) {
+    const int32_t lg = p.logical[flat(pos)];
+    if (lg < 0 || lg >= n) {
+      set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+      continue;
+    }
+    const uint32_t bit = 1u << (lg & 31);
+    if (atomicOr(&bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+  }
+  __syncthreads();
+  // exclusive popcount prefix per word, stored in hist-sized chunks
+  int32_t *wpre = reinterpret_cast<int32_t *>(bitmap) + words;  // second half of the smem window
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < words; base += kThreads) {
+      const int w = base + threadIdx.x;
+      const int32_t c = w < words ? __popc(bitmap[w]) : 0;
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(c, excl, tot);
+      if (w < words) wpre[w] = carry + excl;
+      carry += tot;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int64_t pos = threadIdx.x; pos < Cn; pos += kThreads) {
+    const int64_t f = flat(pos);
+    const int32_t lg = p.logical[f];
+    if (lg < 0 || lg >= n) continue;
+    const uint32_t w = bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u);
+    p.logical[f] = wpre[lg >> 5] + __popc(w);
+  }
+  if (threadIdx.x == 0) {
+    p.nblocks[hidx] = keep;
+    p.ctx[hidx] = Cn;
+    if (M.move_counts) M.move_counts[g] = nmoves;
+    if (M.evicted_kvs) M.evicted_kvs[g] = cnt_s[2];
+    if (M.totals) {
+      atomicAdd((unsigned long long *)&M.totals[0], (unsigned long long)e);
+      atomicAdd((unsigned long long *)&M.totals[1], (unsigned long long)cnt_s[2]);
+      atomicAdd((unsigned long long *)&M.totals[2], (unsigned long long)nmoves);
+    }
+  }
+}
+
+__global__ void k_free_total(kvc_pool p, int64_t *totals) {
+  using Red = cub::BlockReduce<int64_t, 1024>;
+  __shared__ typename Red::TempStorage tmp;
+  int64_t s = 0;
+  for (int t = threadIdx.x; t < num_tiles(&p); t += 1024) s += p.free_tile[t];
+  s = Red(tmp).Sum(s);
+  if (threadIdx.x == 0) totals[3] = s;
+}
+
+int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, EvictState &S) {
+  S.hp = pool->num_layers * pool->num_kv_heads;
+  S.max_slots = a->max_slots_per_head;
+  S.status = pool->status;
+  const int64_t T = (int64_t)a->n_seqs * S.hp;
+  S.keys = sc.take<uint32_t>(T * S.max_slots);
+  S.cap = sc.take<int32_t>(T);
+  S.lo = sc.take<int32_t>(T);
+  S.hi = sc.take<int32_t>(T);
+  S.R = sc.take<int32_t>((int64_t)a->n_seqs * kBins);
+  S.prefix = sc.take<uint32_t>(a->n_seqs);
+  S.E = sc.take<int64_t>(a->n_seqs);
+  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.R || !S.prefix || !S.E) return KVC_ERR_INVALID;
+  return KVC_OK;
+}
+
+int validate(const kvc_pool *pool, const kvc_evict_args *a) {
+  if (!pool || !a || a->n_seqs < 0 || !pool->metric || !pool->tables) return KVC_ERR_INVALID;
+  if (a->n_seqs && (!a->seq_rows || !a->budgets || !a->evict || !a->clamped || !a->move_offsets))
+    return KVC_ERR_INVALID;
+  if (a->max_slots_per_head < 1) return KVC_ERR_INVALID;
+  return KVC_OK;
+}
+
+int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
+  const int64_t T = (int64_t)a->n_seqs * S.hp;
+  cudaMemsetAsync(S.R, 0, (int64_t)a->n_seqs * kBins * sizeof(int32_t), s);
+  k_load<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1);
+  k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 1, 11, a->clamped);
+  k_hist<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11);
+  k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 2, 11, a->clamped);
+  k_hist<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10);
+  k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 3, 10, a->clamped);
+  k_bounds<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, S);
+  k_select<<<1, 1024, 0, s>>>(S, a->n_seqs, pool->block_size, a->evict, a->move_offsets, pool->status);
+  KVC_CHECK_LAUNCH();
+  return KVC_OK;
+}
+
+int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
+  const int64_t T = (int64_t)a->n_seqs * S.hp;
+  if (a->totals) cudaMemsetAsync(a->totals, 0, 4 * sizeof(int64_t), s);
+  MoveArgs M{a->evict, a->evicted_kvs, a->freed, a->moves, a->move_offsets, a->move_counts, a->totals};
+  const int words = (int)((S.max_slots + 31) / 32);
+  const int dyn = words * 8;  // bitmap + word prefixes
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  if (dyn > 200 * 1024) return KVC_ERR_UNSUPPORTED;
+  k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
+  if (a->totals) k_free_total<<<1, 1024, 0, s>>>(*pool, a->totals);
+  KVC_CHECK_LAUNCH();
+  return KVC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kvc_schedule_evictions(const kvc_pool *pool, const kvc_evict_args *a, void *stream) {
+  int rc = validate(pool, a);
+  if (rc || a->n_seqs == 0) return rc;
+  Scratch sc(pool);
+  EvictState S;
+  if ((rc = setup_state(pool, a, sc, S))) return rc;
+  return run_schedule(pool, a, S, (cudaStream_t)stream);
+}
+
+int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *a, void *stream) {
+  int rc = validate(pool, a);
+  if (rc || a->n_seqs == 0) return rc;
+  if (!a->moves || !pool->k_cache) return KVC_ERR_INVALID;
+  Scratch sc(pool);
+  EvictState S;
+  if ((rc = setup_state(pool, a, sc, S))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  // keys are recomputed so the call is self-contained
+  const int64_t T = (int64_t)a->n_seqs * S.hp;
+  k_load<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0);
+  return run_compact(pool, a, S, s);
+}
+
+int kvc_compress(const kvc_pool *pool, const kvc_evict_args *a, void *stream) {
+  int rc = validate(pool, a);
+  if (rc || a->n_seqs == 0) return rc;
+  if (!a->moves || !pool->k_cache) return KVC_ERR_INVALID;
+  Scratch sc(pool);
+  EvictState S;
+  if ((rc = setup_state(pool, a, sc, S))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = run_schedule(pool, a, S, s))) return rc;
+  return run_compact(pool, a, S, s);
+}
+
+}  // extern "C"

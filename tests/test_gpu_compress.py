@@ -1,0 +1,188 @@
+"""K3 schedule + K4 compaction parity against the CPU oracle (GPU).
+
+The bar is bit-exact: schedules (per-head evicted blocks, clamped budgets),
+move lists, freed block ids, block tables, context lengths, logical
+indices, flags and the moved K/V/metric values must equal the oracle run on
+identical inputs (fp32 metrics widened to float64, bf16 KV).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import load
+from gpu_rig import DevRig, bf16_round, f32_round, random_state
+from oracle import kvc_oracle as O
+from oracle_rig import state_from_snapshot
+
+pytestmark = pytest.mark.gpu
+
+import paper_2410_00161_b200 as K  # noqa: E402
+from paper_2410_00161_b200 import _lib  # noqa: E402
+
+
+def assert_state_equal(rig: DevRig, st: O.OracleState):
+    dst = rig.to_oracle()
+    assert {s: t for s, t in dst.tables.items()} == {s: t for s, t in st.tables.items()}
+    for s in st.ctx:
+        assert np.array_equal(dst.ctx[s], st.ctx[s]), s
+    assert np.array_equal(dst.free, st.free)
+    assert np.array_equal(dst.logical, st.logical)
+    assert np.array_equal(dst.protected, st.protected)
+    assert np.array_equal(dst.fresh, st.fresh)
+    assert np.array_equal(dst.metric, st.metric)
+    assert np.array_equal(dst.keys, st.keys)
+    assert np.array_equal(dst.values, st.values)
+
+
+def device_compress(rig, budgets):
+    sched = K.compress(rig.cache, rig.tables, rig.manager, rig.store, budgets)
+    return sched.to_dict()
+
+
+def normalise(st):
+    st.keys = bf16_round(st.keys)
+    st.values = bf16_round(st.values)
+    st.metric = f32_round(st.metric)
+    return st
+
+
+@pytest.mark.parametrize("i", range(len(load("compress_cases.json"))))
+def test_compress_golden(i):
+    """Reference compression rounds: device == oracle(fp32 metrics) exactly, and
+    == the reference's own schedule whenever fp32 rounding keeps its order."""
+    case = load("compress_cases.json")[i]
+    args = (case["num_blocks"], case["block_size"], case["head_dim"], case["layers"], case["heads"])
+    st = normalise(state_from_snapshot(case["before"], *args))
+    rig = DevRig(*args, max_seqs=8)
+    rig.load(st)
+    budgets = {int(s): int(e) for s, e in case["budgets"]}
+    got = device_compress(rig, budgets)
+    want = O.compress(st, budgets)
+    assert got == want
+    assert_state_equal(rig, st)
+    st_ref = state_from_snapshot(case["before"], *args)
+    if O.compress(st_ref, budgets) == want:
+        assert got == case["schedule"]
+
+
+def fuzz_state(rng, b, d, layers, heads, seqs, max_len, kind):
+    nblocks = len(seqs) * layers * heads * (max_len // b + 3) + 32
+    st = random_state(rng, nblocks, b, d, layers, heads, seqs, max_len, metric_kind="iid")
+    for s in seqs:
+        for m in range(layers):
+            for h in range(heads):
+                f = st.live_slots(s, m, h)
+                n = f.size
+                if kind == "pooled":  # runs of equal values, like max-pooled metrics
+                    base = rng.random(n // 3 + 2)
+                    st.metric[f] = f32_round(base[np.arange(n) // 3])
+                elif kind == "ties":
+                    st.metric[f] = f32_round(np.round(rng.random(n), 1))
+                elif kind == "zeros":
+                    st.metric[f] = 0.0
+                if rng.random() < 0.3:
+                    st.protected[f[-min(n, 8):]] = True
+                if rng.random() < 0.2:
+                    st.fresh[f[-1]] = True
+    return st
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_compress_fuzz(seed):
+    rng = np.random.default_rng(1000 + seed)
+    b = int(rng.choice([2, 4, 16]))
+    d = int(rng.choice([8, 16, 64]))
+    layers = int(rng.integers(1, 4))
+    heads = int(rng.integers(1, 5))
+    seqs = list(rng.choice(50, size=int(rng.integers(1, 4)), replace=False))
+    kind = ["iid", "pooled", "ties", "zeros"][seed % 4]
+    st = fuzz_state(rng, b, d, layers, heads, [int(s) for s in seqs], int(rng.integers(b, 12 * b)), kind)
+    rig = DevRig(st.num_blocks, b, d, layers, heads)
+    rig.load(st)
+    for rnd in range(3):
+        budgets = {}
+        for s in st.tables:
+            nb = st.block_count(s)
+            budgets[s] = int(rng.integers(-1, nb + 2))
+        got = device_compress(rig, budgets)
+        want = O.compress(st, budgets)
+        assert got == want, (rnd, budgets)
+        assert_state_equal(rig, st)
+        # regrow every head by a few tokens (acceptance criterion 3 style)
+        for s in st.tables:
+            for m in range(layers):
+                for h in range(heads):
+                    for _ in range(int(rng.integers(0, 3))):
+                        c = int(st.ctx[s][m, h])
+                        if c % b == 0:
+                            if st.free_count == 0:
+                                break
+                            st.tables[s][m][h].extend(int(x) for x in O._take_smallest(st, 1))
+                            rig.manager._take(s, m, h)
+                        k = bf16_round(rng.standard_normal(d))
+                        v = bf16_round(rng.standard_normal(d))
+                        f = O.append(st, s, m, h, k, v, fresh=False)
+                        st.metric[f] = f32_round(rng.random())
+                        hnd = K.append_kv(rig.tables, rig.cache, s, m, h, k, v)
+                        rig.store.on_append(hnd, logical=c)
+                        rig.store.metrics[hnd.block, hnd.offset] = float(st.metric[f])
+        assert_state_equal(rig, st)
+
+
+def test_schedule_then_execute_equals_compress():
+    rng = np.random.default_rng(11)
+    st = fuzz_state(rng, 16, 64, 2, 4, [0, 5], 400, "pooled")
+    rig = DevRig(st.num_blocks, 16, 64, 2, 4)
+    rig.load(st)
+    budgets = {5: 20, 0: 35}
+    plan = K.schedule_evictions(rig.tables, rig.store, budgets, manager=rig.manager)
+    for s, counts in plan.evict_counts().items():
+        clamped, want, _ = O.evict_counts(st, s, budgets[s])
+        assert counts == want
+    assert plan.clamped.cpu().tolist() == [min(budgets[s], O.evict_counts(st, s, budgets[s])[0]) for s in budgets]
+    sched = K.execute_cache_moves(rig.cache, rig.tables, rig.manager, rig.store, plan)
+    assert sched.to_dict() == O.compress(st, budgets)
+    assert_state_equal(rig, st)
+
+
+def test_llama_slice_exact():
+    """Llama-3.1-8B-shaped slice: 2 layers x 8 heads x 4096 tokens, b=16, d=128,
+    pooled (tie-heavy) metrics, compressed 8x in one round."""
+    rng = np.random.default_rng(8)
+    b, d, layers, heads, L = 16, 128, 2, 8, 4096
+    nblocks = layers * heads * (L // b) + 64
+    st = O.OracleState(nblocks, b, d, layers, heads)
+    O.alloc_prefill(st, 0, L)
+    for m in range(layers):
+        for h in range(heads):
+            st.ctx[0][m, h] = L
+            f = st.live_slots(0, m, h)
+            st.keys[f] = bf16_round(rng.standard_normal((L, d)))
+            st.values[f] = bf16_round(rng.standard_normal((L, d)))
+            raw = rng.random(L) ** 3
+            st.metric[f] = f32_round(O.pool_max(raw[None], 7)[0])
+            st.logical[f] = np.arange(L)
+            st.protected[f[-8:]] = True
+    rig = DevRig(nblocks, b, d, layers, heads, max_seqs=2)
+    rig.load(st)
+    E = O.budget_to_blocks(L // 8, layers, heads, b, st.block_count(0))
+    got = device_compress(rig, {0: E})
+    want = O.compress(st, {0: E})
+    assert got == want
+    assert_state_equal(rig, st)
+    assert got["freed_blocks"] == E
+
+
+def test_totals_and_free_count():
+    rng = np.random.default_rng(3)
+    st = fuzz_state(rng, 4, 8, 1, 3, [1, 2], 40, "iid")
+    rig = DevRig(st.num_blocks, 4, 8, 1, 3)
+    rig.load(st)
+    plan = K.compress(rig.cache, rig.tables, rig.manager, rig.store, {1: 5, 2: 3}, sync=False)
+    want = O.compress(st, {1: 5, 2: 3})
+    tot = plan.totals.cpu().tolist()
+    assert tot[0] == want["freed_blocks"] and tot[1] == want["evicted_kvs"]
+    assert tot[3] == st.free_count == rig.manager.free_count
