@@ -1,0 +1,401 @@
+// K2: observation-window importance metric at prefill, on tcgen05 tensor
+// cores with TMA-staged operands.
+//
+// Reference: gqa_attention (pkg/src/pagedkv/attention.py:62-89) builds the
+// full causal softmax; window_metrics (metrics.py:68-89) sums f(A[h,i,j])
+// over the last w query rows i and the r query heads of KV head h, then
+// max-pools along the key axis (metrics.py:57-65) and protects the window;
+// write_prompt_pass installs the result per slot (metrics.py:160-175).
+//
+// Only the r*w window rows of each KV head are ever formed here:
+//   S^T[key, row] = K[key,:] . Q_w[row,:]       (M = 128 keys, N = r*w rows)
+// is one tcgen05.mma.kind::f16 (bf16 in, fp32 accumulate in TMEM) per
+// 16-wide K step; K tiles (128 keys x d) and the Q window are loaded by TMA
+// (SWIZZLE_128B, K-major) into a 4-stage shared-memory ring.  Warp roles:
+// warp 0 TMA producer, warp 1 MMA issuer + TMEM owner, warps 2-5 epilogue
+// (one TMEM lane quadrant each).
+//   pass 0: per-row online (max, sum exp) over this CTA's keys  -> partials
+//   combine: per row M, 1/Z                                      (tiny)
+//   pass 1: recompute the tile, raw[j] = sum_rows f(exp(s-M)/Z)   -> raw
+//           (the layer's K is re-read from L2: 64 MB at Llama-8B shapes)
+//   pool:  centred max-pool, install metric/logical/protected per slot.
+#include <cuda.h>
+
+#include "common.cuh"
+
+using namespace kvc;
+
+namespace {
+
+constexpr int kTileKeys = 128;
+template <int D>
+constexpr int stages_for() { return D >= 256 ? 2 : 4; }
+constexpr int kThreads = 192;  // 6 warps
+
+struct WinParams {
+  int L, H, r, wq, RW, D, start;
+  int tiles_per_head, chunks;  // CTA = (chunk, head)
+  float scale;                 // log2(e) / sqrt(d)
+  int agg;                     // 1 L1, 2 L2
+  float2 *partial;             // [H][chunks][N] (m, z)
+  const float2 *stat;          // [H][N] (M, 1/Z)
+  float *raw;                  // [H][L]
+};
+
+// ---- PTX wrappers ---------------------------------------------------------
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // K-major, SWIZZLE_128B: LBO = 16 B (ignored), SBO = 1024 B (8 rows x 128 B),
+  // descriptor version 1 (sm_100), layout type 2.
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// ---- the tile pipeline ------------------------------------------------------
+
+template <int N, int D, int PASS>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_window(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, const WinParams P) {
+  constexpr int kStages = stages_for<D>();
+  constexpr int kAtoms = D / 64;                      // 128-byte K-major column blocks
+  constexpr int kTileBytes = kTileKeys * D * 2;       // one K tile
+  constexpr int kQBytes = N * D * 2;
+  constexpr uint32_t kCols = 2 * N;                   // two TMEM accumulators
+  constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : 128;
+  constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *ktiles = smem;                                  // kStages x kTileBytes
+  uint8_t *qbuf = smem + kStages * kTileBytes;             // kQBytes
+  float *sbuf = reinterpret_cast<float *>(qbuf + kQBytes);  // pass 0: [128][N+1]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sbuf + kTileKeys * (N + 1));
+  uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2, *qfull = tempty + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qfull + 1);
+  float *stat_s = reinterpret_cast<float *>(tmem_slot + 4);  // pass 1: M[N], invZ[N]
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int chunk = blockIdx.x, head = blockIdx.y;
+  const int t_lo = (int)((int64_t)chunk * P.tiles_per_head / P.chunks);
+  const int t_hi = (int)((int64_t)(chunk + 1) * P.tiles_per_head / P.chunks);
+  const int ntiles = t_hi - t_lo;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    mbar_init(qfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { prefetch_tmap(&tmK); prefetch_tmap(&tmQ); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (PASS == 1) {
+    for (int c = threadIdx.x; c < N; c += kThreads) {
+      const float2 st = P.stat[(int64_t)head * N + c];
+      stat_s[c] = st.x;
+      stat_s[N + c] = st.y;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0 && ntiles > 0) {
+      mbar_expect_tx(qfull, kQBytes);
+      for (int a = 0; a < kAtoms; ++a)
+        tma_load_2d(qbuf + a * N * 128, &tmQ, a * 64, head * P.RW, qfull);
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kTileBytes);
+        const int row = head * P.L + (t_lo + i) * kTileKeys;
+        for (int a = 0; a < kAtoms; ++a)
+          tma_load_2d(ktiles + s * kTileBytes + a * kTileKeys * 128, &tmK, a * 64, row, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (ntiles > 0) {
+      mbar_wait(qfull, 0);
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % kStages, acc = i & 1;
+        mbar_wait(&full[s], (i / kStages) & 1);
+        if (i >= 2) mbar_wait(&tempty[acc], ((i / 2) - 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t abase = smem_u32(ktiles + s * kTileBytes);
+          const uint32_t bbase = smem_u32(qbuf);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const int atom = kk / 4, sub = kk % 4;
+            const uint64_t ad = sw128_desc(abase + atom * kTileKeys * 128 + sub * 32);
+            const uint64_t bd = sw128_desc(bbase + atom * N * 128 + sub * 32);
+            mma_bf16(tmem + acc * N, ad, bd, kIdesc, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);   // smem stage reusable once these MMAs finish
+          mma_commit(&tfull[acc]); // accumulator ready for the epilogue
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5 = TMEM lane quadrants 2,3,0,1) ------
+    const int quad = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    const int key_local = quad * 32 + lane;
+    float m_run = -INFINITY, z_run = 0.f;  // pass 0: this thread's (column, part)
+    constexpr int kParts = 128 / N;        // threads per column
+    const int col = et % N, part = et / N;
+    float raw_part = 0.f;
+    (void)raw_part;
+    for (int i = 0; i < ntiles; ++i) {
+      const int acc = i & 1;
+      mbar_wait(&tfull[acc], (i / 2) & 1);
+      tc_fence_after();
+      float v[N];
+#pragma unroll
+      for (int g = 0; g < N / 32; ++g) tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * N + g * 32, v + g * 32);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);  // 128 arrivals release the accumulator
+      const int j = (t_lo + i) * kTileKeys + key_local;  // key position within the head
+      if (PASS == 0) {
+        float *srow = sbuf + key_local * (N + 1);
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const int ii = c % P.wq;
+          const bool ok = c < P.RW && j < P.L && j <= P.start + ii;
+          srow[c] = ok ? v[c] * P.scale : -INFINITY;
+        }
+        named_sync(1, 128);
+        // column `col`, keys part*(128/kParts) .. : online max / sum
+        constexpr int kSpan = 128 / kParts;
+        for (int k = 0; k < kSpan; ++k) {
+          const float s = sbuf[(part * kSpan + k) * (N + 1) + col];
+          if (s > m_run) {
+            z_run = z_run * exp2f(m_run - s) + 1.f;
+            m_run = s;
+          } else if (s > -INFINITY) {
+            z_run += exp2f(s - m_run);
+          }
+        }
+        named_sync(1, 128);
+      } else {
+        float contrib = 0.f;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const int ii = c % P.wq;
+          const bool ok = c < P.RW && j <= P.start + ii;
+          const float pr = exp2f(v[c] * P.scale - stat_s[c]) * stat_s[N + c];
+          const float f = P.agg == 2 ? pr * pr : pr;
+          contrib += ok ? f : 0.f;
+        }
+        if (j < P.L) P.raw[(int64_t)head * P.L + j] = contrib;
+      }
+    }
+    if (PASS == 0) {
+      // combine the kParts partial (m, z) of each column
+      float2 *red = reinterpret_cast<float2 *>(sbuf);
+      red[et] = make_float2(m_run, z_run);
+      named_sync(1, 128);
+      if (et < N) {
+        float m = -INFINITY, z = 0.f;
+        for (int p2 = 0; p2 < kParts; ++p2) {
+          const float2 q = red[p2 * N + et];
+          if (q.x == -INFINITY) continue;
+          const float mn = fmaxf(m, q.x);
+          z = (m == -INFINITY ? 0.f : z * exp2f(m - mn)) + q.y * exp2f(q.x - mn);
+          m = mn;
+        }
+        P.partial[((int64_t)head * P.chunks + chunk) * N + et] = make_float2(m, z);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+__global__ void k_win_combine(WinParams P, int N, float2 *stat) {
+  const int head = blockIdx.x, c = threadIdx.x;
+  if (c >= N) return;
+  float m = -INFINITY, z = 0.f;
+  for (int k = 0; k < P.chunks; ++k) {
+    const float2 q = P.partial[((int64_t)head * P.chunks + k) * N + c];
+    if (q.x == -INFINITY) continue;
+    const float mn = fmaxf(m, q.x);
+    z = (m == -INFINITY ? 0.f : z * exp2f(m - mn)) + q.y * exp2f(q.x - mn);
+    m = mn;
+  }
+  stat[(int64_t)head * N + c] = make_float2(m, z > 0.f ? 1.f / z : 0.f);
+}
+
+// Centred max-pool (truncated at the edges) + per-slot install.
+__global__ void k_win_pool(kvc_pool p, WinParams P, int row, int layer, int pool, int protect, float *out) {
+  const int head = blockIdx.y;
+  const int half = pool / 2;
+  const float *raw = P.raw + (int64_t)head * P.L;
+  const int64_t hidx = row >= 0 ? head_index(p, row, layer, head) : 0;
+  const int C = row >= 0 ? p.ctx[hidx] : 0;
+  const int b = p.block_size;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.L; j += gridDim.x * blockDim.x) {
+    float m = raw[j];
+    const int lo = j - half < 0 ? 0 : j - half;
+    const int hi = j + half >= P.L ? P.L - 1 : j + half;
+    for (int t = lo; t <= hi; ++t) m = fmaxf(m, raw[t]);
+    if (out) out[(int64_t)head * P.L + j] = m;
+    if (row >= 0 && j < C) {
+      const int64_t f = (int64_t)head_table(p, hidx)[j / b] * b + j % b;
+      p.metric[f] = m;
+      p.logical[f] = j;
+      p.protected_[f] = (protect && j >= P.start) ? 1 : 0;
+      p.fresh[f] = 0;
+    }
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 map over [rows][D] with a {64, box_rows} SWIZZLE_128B box.
+bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N, int D>
+int run_window(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cudaStream_t s) {
+  CUtensorMap tmK, tmQ;
+  if (!make_map(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
+  if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
+  const int smem = stages_for<D>() * kTileKeys * D * 2 + N * D * 2 + kTileKeys * (N + 1) * 4 + 256 + 2 * N * 4 + 1024;
+  auto k0 = k_window<N, D, 0>;
+  auto k1 = k_window<N, D, 1>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  if (smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
+  dim3 grid(P.chunks, P.H);
+  k0<<<grid, kThreads, smem, s>>>(tmK, tmQ, P);
+  float2 *stat = const_cast<float2 *>(P.stat);
+  k_win_combine<<<P.H, 64, 0, s>>>(P, N, stat);
+  k1<<<grid, kThreads, smem, s>>>(tmK, tmQ, P);
+  const int gx = (P.L + 255) / 256 < 1184 ? (P.L + 255) / 256 : 1184;
+  k_win_pool<<<dim3(gx, P.H), 256, 0, s>>>(*pool, P, a->seq_row, a->layer, a->pool, a->protect_window,
+                                           a->metrics_out);
+  KVC_CHECK_LAUNCH();
+  return KVC_OK;
+}
+
+}  // namespace
+
+extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a, void *stream) {
+  if (!pool || !a || !a->q_win || !a->k || a->L < 1 || a->window < 1 || a->pool < 1 || a->pool % 2 == 0)
+    return KVC_ERR_INVALID;
+  const int H = pool->num_kv_heads;
+  const int D = pool->head_dim;
+  if (a->num_query_heads % H) return KVC_ERR_INVALID;
+  if (a->seq_row >= 0 && (!pool->metric || !pool->tables)) return KVC_ERR_INVALID;
+  WinParams P;
+  P.L = a->L;
+  P.H = H;
+  P.r = a->num_query_heads / H;
+  P.wq = a->window < a->L ? a->window : a->L;
+  P.RW = P.r * P.wq;
+  P.D = D;
+  P.start = a->L - P.wq;
+  P.tiles_per_head = (a->L + kTileKeys - 1) / kTileKeys;
+  int chunks = (148 + H - 1) / H;
+  if (chunks > P.tiles_per_head) chunks = P.tiles_per_head;
+  P.chunks = chunks;
+  P.scale = 1.4426950408889634f / sqrtf((float)D);
+  P.agg = a->aggregation == 2 ? 2 : 1;
+  const int N = P.RW <= 32 ? 32 : P.RW <= 64 ? 64 : 0;
+  if (!N) return KVC_ERR_UNSUPPORTED;
+  Scratch sc(pool);
+  P.partial = sc.take<float2>((int64_t)H * chunks * N);
+  P.stat = sc.take<float2>((int64_t)H * N);
+  P.raw = sc.take<float>((int64_t)H * a->L);
+  if (!P.partial || !P.stat || !P.raw) return KVC_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (N == 32 && D == 64) return run_window<32, 64>(pool, a, P, s);
+  if (N == 32 && D == 128) return run_window<32, 128>(pool, a, P, s);
+  if (N == 32 && D == 256) return run_window<32, 256>(pool, a, P, s);
+  if (N == 64 && D == 64) return run_window<64, 64>(pool, a, P, s);
+  if (N == 64 && D == 128) return run_window<64, 128>(pool, a, P, s);
+  return KVC_ERR_UNSUPPORTED;
+}

@@ -1,9 +1,121 @@
-"""Prefill write path + observation-window metric (K2) -- under construction."""
+"""Prefill write path and observation-window metric (K2).
+
+The reference engine's prefill (pkg/src/pagedkv/engine.py:335-358) scatters a
+prompt's K/V into every head's blocks, builds the full (n_q, L, L) causal
+attention (attention.py:62-89), reduces it to window metrics
+(metrics.py:68-89) and installs them per slot (metrics.py:160-175).  Here
+the K/V scatter is one vectorised kernel per layer and the metric is K2
+(csrc/window.cu): only the last w query rows are multiplied against K on
+tcgen05 tensor cores, and the pooled result is written straight into the
+metrics store through the block table.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .attention import AttentionConfig
+from .block_manager import BlockManager
+from .cache import BlockTables, UnifiedKVCache, pool_struct, with_scratch
+from .errors import ConfigError
+from .metrics import WINDOW, MetricConfig, MetricsStore
 
 
-def window_metrics(*a, **k):
-    raise NotImplementedError
+def _dev_bf16(x, dev) -> torch.Tensor:
+    if not torch.is_tensor(x):
+        x = torch.as_tensor(np.asarray(x))
+    return x.to(dev, torch.bfloat16).contiguous()
 
 
-def prefill_sequence(*a, **k):
-    raise NotImplementedError
+def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev, pool_p=None,
+                 seq_row: int = -1, layer: int = 0, metrics_out=None) -> None:
+    n_q, L = q.shape[0], k.shape[1]
+    w = min(cfg.window, L)
+    q_win = q[:, L - w:, :] if q.shape[1] == L else q
+    if q_win.shape[1] != w:
+        raise ValueError(f"query window has {q_win.shape[1]} rows, expected {w}")
+    q_win = q_win.contiguous()
+    a = _lib.WindowArgs()
+    a.seq_row = seq_row
+    a.layer = layer
+    a.num_query_heads = n_q
+    a.L = L
+    a.q_win = q_win.data_ptr()
+    a.k = k.data_ptr()
+    a.window = cfg.window
+    a.pool = cfg.pool
+    a.aggregation = cfg.metric_mode
+    a.protect_window = int(cfg.protect_window)
+    a.metrics_out = _lib.ptr(metrics_out)
+    if pool_p is None:
+        pool_p = _lib.KvcPool()
+        pool_p.status = _lib.DeviceContext.get(dev).status.data_ptr()
+    pool_p.num_kv_heads = num_kv_heads
+    pool_p.head_dim = head_dim
+    with_scratch(pool_p, dev, num_kv_heads * (L * 4 + 64 * 8 * 200) + (1 << 16))
+    _lib.check(_lib.lib().kvc_window_metric(ctypes.byref(pool_p), ctypes.byref(a), _lib.stream_ptr(dev)),
+               "window_metric")
+
+
+def window_metrics(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
+    """Observation-window metrics of one layer from its prompt Q and K.
+
+    q: (n_q, L, d) or just the last min(w, L) query rows (n_q, w', d);
+    k: (num_kv_heads, L, d).  Returns (metrics (num_kv_heads, L) fp32 tensor,
+    protected (L,) bool tensor) like pagedkv.metrics.window_metrics, which the
+    reference computes from the full attention tensor (metrics.py:68-89).
+    """
+    dev = _lib.require_cuda(device if device is not None else (q.device if torch.is_tensor(q) and q.is_cuda else None))
+    qt, kt = _dev_bf16(q, dev), _dev_bf16(k, dev)
+    L = kt.shape[1]
+    out = torch.empty((num_kv_heads, L), dtype=torch.float32, device=dev)
+    _window_call(qt, kt, cfg, num_kv_heads, kt.shape[2], dev, metrics_out=out)
+    start = max(L - cfg.window, 0)
+    protected = torch.arange(L, device=dev) >= start
+    if not cfg.protect_window:
+        protected[:] = False
+    return out, protected
+
+
+def write_prefill_kv(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, layer: int, k, v) -> None:
+    """Scatter one layer's prompt K/V (heads, L, d) into the head tables; C := L."""
+    dev = cache.device
+    kt, vt = _dev_bf16(k, dev), _dev_bf16(v, dev)
+    L = kt.shape[1]
+    p = pool_struct(cache=cache, tables=tables)
+    _lib.check(_lib.lib().kvc_write_prefill_kv(ctypes.byref(p), tables.row(seq_id), layer, kt.data_ptr(),
+                                               vt.data_ptr(), L, _lib.stream_ptr(dev)), "write_prefill_kv")
+    row = tables.row(seq_id)
+    tables.ctx_bound[row] = max(tables.ctx_bound[row], L)
+
+
+def prefill_layer(cache: UnifiedKVCache, tables: BlockTables, store: MetricsStore, seq_id: int, layer: int,
+                  q, k, v, cfg: MetricConfig) -> None:
+    """One layer of the engine prefill: scatter K/V, window metric, install
+    (engine.py:340-353).  Asynchronous."""
+    if cfg.mode != WINDOW:
+        raise ConfigError("mode", "the device prefill metric implements the observation window")
+    dev = cache.device
+    write_prefill_kv(cache, tables, seq_id, layer, k, v)
+    qt, kt = _dev_bf16(q, dev), _dev_bf16(k, dev)
+    p = pool_struct(cache=cache, tables=tables, store=store)
+    _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
+                 seq_row=tables.row(seq_id), layer=layer)
+
+
+def prefill_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
+                     seq_id: int, q, k, v, cfg: MetricConfig, attn: AttentionConfig | None = None) -> int:
+    """Allocate + write + score a prompt: q (l, n_q, L or w, d), k/v (l, H, L, d).
+
+    Raises PreemptionNeeded (nothing allocated) when the pool is short.
+    Returns the number of blocks allocated.
+    """
+    L = k.shape[2]
+    demand = manager.allocate_prefill(seq_id, L)
+    for layer in range(tables.num_layers):
+        prefill_layer(cache, tables, store, seq_id, layer, q[layer], k[layer], v[layer], cfg)
+    return demand
