@@ -175,6 +175,12 @@ typedef struct kvc_decode_args {
 
 int kvc_paged_decode(const kvc_pool *pool, const kvc_decode_args *args, void *stream);
 
+/* Workspace the decode fast path needs for `batch` sequences with contexts
+ * up to `max_ctx` (fp32 score rows + split-KV partials).  With less scratch
+ * kvc_paged_decode uses the single-pass cluster kernel. */
+int64_t kvc_decode_scratch_bytes(const kvc_pool *pool, int32_t batch, int32_t num_query_heads,
+                                 int32_t max_ctx);
+
 /* metric[slot_j] += sum_h f(rows[h][j]) for one (row, layer): rows f32
  * [heads][r][rows_stride] covering each head's C live KVs. */
 int kvc_accumulate_rows(const kvc_pool *pool, int32_t seq_row, int32_t layer,

@@ -88,6 +88,7 @@ _SIGS = {
     "kvc_write_prefill_kv": ([_p, _i32, _i32, _p, _p, _i32, _p], _i32),
     "kvc_write_prompt_pass": ([_p, _i32, _i32, _p, _i64, _p, _i32, _p], _i32),
     "kvc_paged_decode": ([_p, _p, _p], _i32),
+    "kvc_decode_scratch_bytes": ([_p, _i32, _i32, _i32], _i64),
     "kvc_accumulate_rows": ([_p, _i32, _i32, _p, _i32, _i64, _i32, _p], _i32),
     "kvc_clear_fresh": ([_p, _p, _i32, _p], _i32),
     "kvc_window_metric": ([_p, _p, _p], _i32),

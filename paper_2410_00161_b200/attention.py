@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .cache import BlockTables, UnifiedKVCache, pool_struct
+from .cache import BlockTables, UnifiedKVCache, pool_struct, with_scratch
 from .errors import NumericError
 
 
@@ -90,6 +90,8 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     a.max_ctx = max(1, int(max_ctx))
     a.splits = splits
     p = pool_struct(cache=cache, tables=tables, store=store)
+    need = _lib.lib().kvc_decode_scratch_bytes(ctypes.byref(p), B, cfg.num_query_heads, a.max_ctx)
+    with_scratch(p, dev, need)
     _lib.check(_lib.lib().kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)),
                "paged_decode")
     return out

@@ -29,6 +29,8 @@
 namespace cg = cooperative_groups;
 using namespace kvc;
 
+int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int splits, int chunk, cudaStream_t s);
+
 namespace {
 
 constexpr int kWarps = 4;
@@ -582,6 +584,11 @@ int kvc_paged_decode(const kvc_pool *pool, const kvc_decode_args *a, void *strea
   const int rm = rmax_of(r);
   // splits: enough CTAs to fill 148 SMs ~4 deep, >= 256 positions per CTA,
   // and a score buffer that fits shared memory.
+  // tensor-core persistent fast path (block_size 16, d in {64,128,256}, r <= 8)
+  {
+    const int rc = kvc_decode_mma(pool, a, 0, 0, (cudaStream_t)stream);
+    if (rc != KVC_ERR_UNSUPPORTED) return rc;
+  }
   int splits = a->splits;
   if (splits <= 0) {
     const int64_t pairs = (int64_t)a->batch * H;

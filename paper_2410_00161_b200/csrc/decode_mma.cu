@@ -1,0 +1,633 @@
+// K1 fast path: paged GQA decode on tensor cores, persistent + split-KV
+// (block_size 16, head_dim 64/128/256, group size <= 8).  Same semantics as
+// k_paged_decode in decode.cu (reference: attention.py:92-127, metrics.py:
+// 189-211, cache.py:163-184, engine.py:426-444).
+//
+// Kernel A (k_decode_stream): a persistent grid (2 CTAs per SM) pulls work
+// items = (sequence, KV head, 512-position chunk) from an atomic queue
+// (largest-position chunks last).  Each of the 4 warps streams its 16-token
+// blocks of the item through a private TMA ring (cp.async.bulk.tensor,
+// SWIZZLE_128B, one op for K and one for V per block) and runs
+//   S^T[16 tok x 8 heads] = K . Q^T       d/16 x mma.m16n8k16 (bf16, fp32 acc)
+//   online softmax per head
+//   O^T[d x 8 heads]    += V^T . P^T      d/16 x mma.m16n8k16, P^T by movmatrix
+// writing the fp32 scores of every position to a scratch row.  The warps'
+// (m, l, O) are merged in shared memory into one partial per item.  The ring
+// keeps streaming across item boundaries (the next item is fetched ahead).
+// Kernel B (k_decode_finish): per (sequence, KV head) merges the partials
+// (log-sum-exp), writes the output, and folds f(exp(s - M) / Z) into the
+// metric of every attended slot (the appended slot is initialised: metric,
+// logical = C, fresh), then C += 1.  Scores are 16 B/position against the
+// 512 B/position of K+V, so the metric costs ~6% extra traffic and no
+// grid-wide synchronisation.
+#include <cuda.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+using namespace kvc;
+
+namespace kvc_mma {
+
+constexpr int kNW = 4;           // warps per CTA
+constexpr int kThreads = kNW * 32;
+constexpr int kBlk = 16;         // tokens per KV block
+constexpr int kHP = 8;           // heads per MMA (group padded to 8)
+constexpr int kItemBlocks = 32;  // blocks per work item (512 positions)
+constexpr int kItemTok = kItemBlocks * kBlk;
+
+struct Params {
+  kvc_pool p;
+  const int32_t *rows;
+  int batch, layer, r;
+  const uint16_t *q, *k_new, *v_new;
+  void *out;
+  int out_f32;
+  float *rows_out;
+  int64_t rows_stride;
+  int metric_mode, append_fresh, stages;
+  int max_ctx_pad;  // score row length per (sequence, head)
+  int n_ck;         // chunks per (sequence, head) upper bound
+  int n_items;
+  float scale;      // log2(e)/sqrt(d)
+  int *counter;     // work queue head (zeroed by kernel B for the next call)
+  float *scores;    // [pairs][max_ctx_pad][r]
+  float *part_ml;   // [pairs][n_ck][2][kHP]
+  float *part_o;    // [pairs][n_ck][r][D]
+};
+
+__device__ __forceinline__ void tma3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar,
+                                      uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void mma16816(float *c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// byte offset of 16-byte chunk `c` of row `row` in a TMA SWIZZLE_128B block
+// laid out as (d/64) atoms of 16 rows x 128 bytes.
+__device__ __forceinline__ uint32_t swz(int row, int c) {
+  return (uint32_t)((c >> 3) * (kBlk * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+}
+
+// Item descriptor shared by the CTA's warps.
+struct Item {
+  int id;        // -1 = none
+  int bi, head;
+  int t0, t1;    // positions [t0, t1) of the head in this item
+  int c_old;     // context before the append
+  int hidx_lo;   // low 32 bits of the head index (tables)
+};
+
+__device__ void decode_item(const Params &P, int id, Item &it) {
+  const kvc_pool &p = P.p;
+  const int H = p.num_kv_heads;
+  const int pairs = P.batch * H;
+  it.id = -1;
+  while (id < P.n_items) {
+    const int ck = id / pairs, pair = id % pairs;
+    const int bi = pair / H, head = pair % H;
+    const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
+    const int c_old = p.ctx[hidx];
+    const int cp = c_old + (P.k_new ? 1 : 0);
+    const int t0 = ck * kItemTok;
+    if (t0 < cp && cp <= p.nblocks[hidx] * kBlk) {
+      it.id = id;
+      it.bi = bi;
+      it.head = head;
+      it.t0 = t0;
+      it.t1 = min(cp, t0 + kItemTok);
+      it.c_old = c_old;
+      it.hidx_lo = (int)hidx;
+      return;
+    }
+    return;  // empty chunk: caller fetches again
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) k_decode_stream(const __grid_constant__ CUtensorMap tmK,
+                                                              const __grid_constant__ CUtensorMap tmV,
+                                                              const Params P) {
+  constexpr int kBlkBytes = kBlk * D * 2;
+  constexpr int kStageBytes = 2 * kBlkBytes;
+  constexpr int kKS = D / 16;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stages = P.stages;
+  uint8_t *ring = smem;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(ring + kNW * stages * kStageBytes);
+  float *wml = reinterpret_cast<float *>(bars + kNW * stages);  // [kNW][2][kHP]
+  float *wo = wml + kNW * 2 * kHP;                              // [kNW][kHP][D]
+  Item *items = reinterpret_cast<Item *>(wo + kNW * kHP * D);   // [2] current / next
+  const kvc_pool &p = P.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int H = p.num_kv_heads, r = P.r, n_q = H * r;
+  const bool append = P.k_new != nullptr;
+
+  uint8_t *my_ring = ring + warp * stages * kStageBytes;
+  uint64_t *my_bars = bars + warp * stages;
+  if (lane == 0)
+    for (int s = 0; s < stages; ++s) mbar_init(&my_bars[s], 1);
+  fence_barrier_init();
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+    // fetch the first two non-empty items
+    for (int k = 0; k < 2; ++k) {
+      Item it;
+      it.id = -1;
+      while (true) {
+        const int id = atomicAdd(P.counter, 1);
+        if (id >= P.n_items) break;
+        decode_item(P, id, it);
+        if (it.id >= 0) break;
+      }
+      items[k] = it;
+    }
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const int32_t *tables = p.tables;
+
+  // Per-warp block stream over (current item, next item): blocks w, w+kNW, ...
+  // of each item.  `issued` counts ring fills, `done` ring drains.
+  int cur = 0;  // items[cur] is the item being computed
+  int issue_item = 0, issue_k = 0;  // next block to issue: items[(cur+issue_item)&1], k-th of this warp
+  int issued = 0, done = 0;
+  auto my_nblocks = [&](const Item &it) {
+    if (it.id < 0) return 0;
+    const int nblk = (it.t1 - 1) / kBlk - it.t0 / kBlk + 1;
+    return nblk > warp ? (nblk - warp + kNW - 1) / kNW : 0;
+  };
+  auto try_issue = [&]() {
+    // lane 0 only: keep `stages` fills ahead across the two visible items
+    while (issued - done < stages && issue_item < 2) {
+      const Item &it = items[(cur + issue_item) & 1];
+      const int nb = my_nblocks(it);
+      if (issue_k >= nb) {
+        if (issue_item == 0 && it.id >= 0) { issue_item = 1; issue_k = 0; continue; }
+        break;
+      }
+      const int blk = it.t0 / kBlk + warp + issue_k * kNW;
+      const int y = tables[(int64_t)it.hidx_lo * p.max_blocks + blk] * kBlk;
+      const int s = issued % stages;
+      uint8_t *dst = my_ring + s * kStageBytes;
+      fence_proxy_async();
+      mbar_expect_tx(&my_bars[s], kStageBytes);
+      tma3d(dst, &tmK, 0, y, 0, &my_bars[s], pol);
+      tma3d(dst + kBlkBytes, &tmV, 0, y, 0, &my_bars[s], pol);
+      ++issued;
+      ++issue_k;
+    }
+  };
+  if (lane == 0) try_issue();
+
+  const int lm_tok = (lane & 7) + ((lane >> 3) & 1) * 8;
+  const int lm_cadd = lane >> 4;
+  const int lt_tok = (lane & 7) + (lane >> 4) * 8;
+  const int lt_cadd = (lane >> 3) & 1;
+  const bool hv0 = 2 * t < r, hv1 = 2 * t + 1 < r;
+
+  while (items[cur].id >= 0) {
+    const Item it = items[cur];
+    const int pair = it.bi * H + it.head;
+    // Q^T B-fragments of this item's query group
+    uint32_t qb[kKS][2];
+    {
+      const bool real = g < r;
+      const uint16_t *qrow = P.q + ((int64_t)it.bi * n_q + it.head * r + (real ? g : 0)) * D;
+#pragma unroll
+      for (int kk = 0; kk < kKS; ++kk) {
+        qb[kk][0] = real ? *reinterpret_cast<const uint32_t *>(qrow + kk * 16 + 2 * t) : 0u;
+        qb[kk][1] = real ? *reinterpret_cast<const uint32_t *>(qrow + kk * 16 + 8 + 2 * t) : 0u;
+      }
+    }
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float oacc[kKS][4];
+#pragma unroll
+    for (int i = 0; i < kKS; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+    float *srow_base = P.scores + (int64_t)pair * P.max_ctx_pad * r;
+    const int nb_me = my_nblocks(it);
+    for (int k = 0; k < nb_me; ++k) {
+      const int s = done % stages;
+      mbar_wait(&my_bars[s], (done / stages) & 1);
+      uint8_t *kb = my_ring + s * kStageBytes;
+      uint8_t *vb = kb + kBlkBytes;
+      const int blk = it.t0 / kBlk + warp + k * kNW;
+      const int tb0 = blk * kBlk;
+      const int valid = min(kBlk, it.t1 - tb0);
+      if (append && it.c_old >= tb0 && it.c_old < tb0 + kBlk) {
+        const int off = it.c_old - tb0;
+        const int64_t slot = (int64_t)tables[(int64_t)it.hidx_lo * p.max_blocks + blk] * kBlk + off;
+        const uint4 *kn = reinterpret_cast<const uint4 *>(P.k_new + ((int64_t)it.bi * H + it.head) * D);
+        const uint4 *vn = reinterpret_cast<const uint4 *>(P.v_new + ((int64_t)it.bi * H + it.head) * D);
+        for (int c = lane; c < D / 8; c += 32) {
+          const uint4 kv = kn[c], vv = vn[c];
+          *reinterpret_cast<uint4 *>(kb + swz(off, c)) = kv;
+          *reinterpret_cast<uint4 *>(vb + swz(off, c)) = vv;
+          reinterpret_cast<uint4 *>(p.k_cache)[slot * (D / 8) + c] = kv;
+          reinterpret_cast<uint4 *>(p.v_cache)[slot * (D / 8) + c] = vv;
+        }
+        __syncwarp();
+      }
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint32_t kbase = smem_u32(kb);
+#pragma unroll
+      for (int kk = 0; kk < kKS; ++kk) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(kbase + swz(lm_tok, 2 * kk + lm_cadd), a0, a1, a2, a3);
+        mma16816(sc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+      }
+      const bool tv0 = g < valid, tv1 = g + 8 < valid;
+      const float s00 = (tv0 && hv0) ? sc[0] * P.scale : -INFINITY;
+      const float s01 = (tv0 && hv1) ? sc[1] * P.scale : -INFINITY;
+      const float s10 = (tv1 && hv0) ? sc[2] * P.scale : -INFINITY;
+      const float s11 = (tv1 && hv1) ? sc[3] * P.scale : -INFINITY;
+      {
+        float *r0 = srow_base + (int64_t)(tb0 + g) * r;
+        float *r1 = r0 + 8 * r;
+        if (tv0 && hv0) r0[2 * t] = s00;
+        if (tv0 && hv1) r0[2 * t + 1] = s01;
+        if (tv1 && hv0) r1[2 * t] = s10;
+        if (tv1 && hv1) r1[2 * t + 1] = s11;
+      }
+      float bm0 = fmaxf(s00, s10), bm1 = fmaxf(s01, s11);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+      }
+      const float mn0 = fmaxf(m0, bm0), mn1 = fmaxf(m1, bm1);
+      const bool z0 = mn0 == -INFINITY, z1 = mn1 == -INFINITY;
+      const float al0 = z0 ? 1.f : exp2f(m0 - mn0);
+      const float al1 = z1 ? 1.f : exp2f(m1 - mn1);
+      const float p00 = z0 ? 0.f : exp2f(s00 - mn0);
+      const float p10 = z0 ? 0.f : exp2f(s10 - mn0);
+      const float p01 = z1 ? 0.f : exp2f(s01 - mn1);
+      const float p11 = z1 ? 0.f : exp2f(s11 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      l0 = l0 * al0 + p00 + p10;
+      l1 = l1 * al1 + p01 + p11;
+      const uint32_t pb0 = movmatrix_t(pack_bf16(p00, p01));
+      const uint32_t pb1 = movmatrix_t(pack_bf16(p10, p11));
+      const uint32_t vbase = smem_u32(vb);
+#pragma unroll
+      for (int mt = 0; mt < kKS; ++mt) {
+        oacc[mt][0] *= al0;
+        oacc[mt][1] *= al1;
+        oacc[mt][2] *= al0;
+        oacc[mt][3] *= al1;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vbase + swz(lt_tok, 2 * mt + lt_cadd), a0, a1, a2, a3);
+        mma16816(oacc[mt], a0, a1, a2, a3, pb0, pb1);
+      }
+      __syncwarp();
+      ++done;
+      if (lane == 0) try_issue();
+    }
+    // ---- merge the warps' (m, l, O) into this item's partial ----
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    if (g == 0) {
+      wml[(warp * 2) * kHP + 2 * t] = m0;
+      wml[(warp * 2) * kHP + 2 * t + 1] = m1;
+      wml[(warp * 2 + 1) * kHP + 2 * t] = l0;
+      wml[(warp * 2 + 1) * kHP + 2 * t + 1] = l1;
+    }
+#pragma unroll
+    for (int mt = 0; mt < kKS; ++mt) {
+      float *w0 = wo + (warp * kHP + 2 * t) * D + mt * 16;
+      float *w1 = wo + (warp * kHP + 2 * t + 1) * D + mt * 16;
+      w0[g] = oacc[mt][0];
+      w1[g] = oacc[mt][1];
+      w0[g + 8] = oacc[mt][2];
+      w1[g + 8] = oacc[mt][3];
+    }
+    __syncthreads();
+    const int ck = it.t0 / kItemTok;
+    float *pml = P.part_ml + ((int64_t)pair * P.n_ck + ck) * 2 * kHP;
+    float *po = P.part_o + ((int64_t)pair * P.n_ck + ck) * r * D;
+    for (int e = threadIdx.x; e < r * D; e += kThreads) {
+      const int h = e / D;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, wml[(w * 2) * kHP + h]);
+      float o = 0.f;
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) {
+        const float mw = wml[(w * 2) * kHP + h];
+        if (mw != -INFINITY) o += wo[(w * kHP + h) * D + (e % D)] * exp2f(mw - mx);
+      }
+      po[e] = o;
+    }
+    if (threadIdx.x < kHP) {
+      const int h = threadIdx.x;
+      float mx = -INFINITY, l = 0.f;
+      for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, wml[(w * 2) * kHP + h]);
+      for (int w = 0; w < kNW; ++w) {
+        const float mw = wml[(w * 2) * kHP + h];
+        if (mw != -INFINITY) l += wml[(w * 2 + 1) * kHP + h] * exp2f(mw - mx);
+      }
+      pml[h] = mx;
+      pml[kHP + h] = l;
+    }
+    // advance: next item becomes current; fetch a new next
+    if (threadIdx.x == 0) {
+      Item nx;
+      nx.id = -1;
+      if (items[cur ^ 1].id >= 0) {
+        while (true) {
+          const int id = atomicAdd(P.counter, 1);
+          if (id >= P.n_items) break;
+          decode_item(P, id, nx);
+          if (nx.id >= 0) break;
+        }
+      }
+      items[cur] = nx;  // slot of the finished item now holds the one after next
+    }
+    __syncthreads();
+    cur ^= 1;
+    // the issue window moves with `cur`
+    if (issue_item == 1) {
+      issue_item = 0;
+    } else {
+      issue_item = 0;
+      issue_k = 0;
+    }
+    if (lane == 0) try_issue();
+  }
+}
+
+// Kernel B: per (sequence, head): merge partials, output, metric, C += 1.
+template <int D>
+__global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
+  extern __shared__ float sm[];
+  float *Ms = sm, *iZ = sm + kHP, *fac = sm + 2 * kHP;  // fac: [n_ck][kHP]
+  const kvc_pool &p = P.p;
+  const int pair = blockIdx.x;
+  const int H = p.num_kv_heads, r = P.r, n_q = H * r;
+  const int bi = pair / H, head = pair % H;
+  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
+  const int c_old = p.ctx[hidx];
+  const bool append = P.k_new != nullptr;
+  const int cp = c_old + (append ? 1 : 0);
+  {
+    // NumericError: non-finite query (attention.py:33-36, 108)
+    const uint16_t *qg = P.q + ((int64_t)bi * n_q + head * r) * D;
+    bool bad = false;
+    for (int e = threadIdx.x; e < r * D; e += blockDim.x) bad |= !isfinite(bf16_bits_to_f32(qg[e]));
+    if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
+  }
+  if (cp < 1 || cp > p.nblocks[hidx] * kBlk) {
+    if (threadIdx.x == 0) {
+      if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
+      else if (append) set_status(p.status, KVC_DEV_ALLOCATION_ORDER, (int32_t)hidx, c_old);
+      else set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, cp);
+    }
+    return;
+  }
+  const int nck = (cp + kItemTok - 1) / kItemTok;
+  const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
+  if (threadIdx.x < kHP) {
+    const int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int c = 0; c < nck; ++c) M = fmaxf(M, pml[c * 2 * kHP + h]);
+    float Z = 0.f;
+    for (int c = 0; c < nck; ++c) {
+      const float m = pml[c * 2 * kHP + h];
+      const float f = m == -INFINITY ? 0.f : exp2f(m - M);
+      fac[c * kHP + h] = f;
+      Z += pml[c * 2 * kHP + kHP + h] * f;
+    }
+    Ms[h] = M;
+    iZ[h] = Z > 0.f ? 1.f / Z : 0.f;
+  }
+  __syncthreads();
+  // output
+  const float *po = P.part_o + (int64_t)pair * P.n_ck * r * D;
+  for (int e = threadIdx.x; e < r * D; e += blockDim.x) {
+    const int h = e / D;
+    float s = 0.f;
+    for (int c = 0; c < nck; ++c) s += po[(int64_t)c * r * D + e] * fac[c * kHP + h];
+    const float o = s * iZ[h];
+    const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
+    if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
+    else reinterpret_cast<__nv_bfloat16 *>(P.out)[oi] = __float2bfloat16(o);
+  }
+  // metric / rows over all attended positions
+  const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
+  const int32_t *tab = head_table(p, hidx);
+  if (P.metric_mode || P.rows_out) {
+    for (int pos = threadIdx.x; pos < cp; pos += blockDim.x) {
+      float contrib = 0.f;
+      for (int h = 0; h < r; ++h) {
+        const float w = exp2f(srow[(int64_t)pos * r + h] - Ms[h]) * iZ[h];
+        contrib += P.metric_mode == 2 ? w * w : w;
+        if (P.rows_out) P.rows_out[(((int64_t)bi * H + head) * r + h) * P.rows_stride + pos] = w;
+      }
+      if (P.metric_mode) {
+        const int64_t slot = (int64_t)tab[pos / kBlk] * kBlk + pos % kBlk;
+        if (append && pos == c_old) {
+          p.metric[slot] = contrib;
+          p.logical[slot] = c_old;
+          p.protected_[slot] = 0;
+          p.fresh[slot] = P.append_fresh ? 1 : 0;
+        } else {
+          p.metric[slot] += contrib;
+        }
+      }
+    }
+  }
+  if (append && !P.metric_mode && p.metric && threadIdx.x == 0) {
+    const int64_t slot = (int64_t)tab[c_old / kBlk] * kBlk + c_old % kBlk;
+    p.metric[slot] = 0.f;
+    p.logical[slot] = c_old;
+    p.protected_[slot] = 0;
+    p.fresh[slot] = P.append_fresh ? 1 : 0;
+  }
+  __syncthreads();
+  if (append && threadIdx.x == 0) p.ctx[hidx] = c_old + 1;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// Cached 3-D SWIZZLE_128B map over a [num_blocks*16, d] bf16 pool viewed as
+// {64 elems, rows, d/64 atoms}; the box {64, 16, d/64} is one whole block.
+static bool pool_map(CUtensorMap *out, const void *base, int64_t rows, int D) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, CUtensorMap> cache;
+  const uint64_t key = reinterpret_cast<uint64_t>(base) * 1315423911ull ^ ((uint64_t)rows << 8) ^ (uint64_t)D;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(D / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)kBlk, (cuuint32_t)(D / 64)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[key] = *out;
+  return true;
+}
+
+int stream_smem(int D, int stages) {
+  return kNW * stages * 2 * kBlk * D * 2 + kNW * stages * 8 + kNW * 2 * kHP * 4 + kNW * kHP * D * 4 +
+         2 * (int)sizeof(Item) + 1024 + 64;
+}
+
+template <int D>
+int launch(Params &P, cudaStream_t s) {
+  CUtensorMap tmK, tmV;
+  const int64_t rows = P.p.num_blocks * kBlk;
+  if (!pool_map(&tmK, P.p.k_cache, rows, D) || !pool_map(&tmV, P.p.v_cache, rows, D)) return KVC_ERR_CUDA;
+  P.stages = D >= 256 ? 2 : 3;
+  const int smem = stream_smem(D, P.stages);
+  auto fa = k_decode_stream<D>;
+  auto fb = k_decode_finish<D>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    configured = true;
+  }
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fa, kThreads, smem);
+  if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
+  int grid = n_sm * per_sm;
+  if (grid > P.n_items) grid = P.n_items;
+  cudaMemsetAsync(P.counter, 0, sizeof(int), s);
+  fa<<<grid, kThreads, smem, s>>>(tmK, tmV, P);
+  const int smem_b = (2 + P.n_ck) * kHP * 4;
+  if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
+  fb<<<P.batch * P.p.num_kv_heads, 256, smem_b, s>>>(P);
+  return cudaGetLastError() == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
+}
+
+}  // namespace kvc_mma
+
+// Workspace bytes the fast path needs (scores + partials + queue head).
+static int64_t kvc_decode_mma_scratch(const kvc_pool *pool, int batch, int r, int max_ctx) {
+  using namespace kvc_mma;
+  const int64_t pairs = (int64_t)batch * pool->num_kv_heads;
+  const int64_t ctxp = ((int64_t)max_ctx + kItemTok - 1) / kItemTok * kItemTok;
+  const int64_t nck = ctxp / kItemTok;
+  return 256 + pairs * ctxp * r * 4 + pairs * nck * 2 * kHP * 4 + pairs * nck * r * pool->head_dim * 4 + 4096;
+}
+
+extern "C" int64_t kvc_decode_scratch_bytes(const kvc_pool *pool, int32_t batch, int32_t num_query_heads,
+                                            int32_t max_ctx) {
+  if (!pool || pool->num_kv_heads < 1) return 0;
+  const int r = num_query_heads / pool->num_kv_heads;
+  return kvc_decode_mma_scratch(pool, batch, r < 1 ? 1 : r, max_ctx > 0 ? max_ctx : 1);
+}
+
+// Returns KVC_ERR_UNSUPPORTED when the shape is outside the fast path.
+int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cudaStream_t s) {
+  using namespace kvc_mma;
+  const int H = pool->num_kv_heads, D = pool->head_dim;
+  const int r = a->num_query_heads / H;
+  if (pool->block_size != kBlk || r > kHP || (D != 64 && D != 128 && D != 256)) return KVC_ERR_UNSUPPORTED;
+  if (!pool->scratch) return KVC_ERR_UNSUPPORTED;
+  const int max_ctx = a->max_ctx > 0 ? a->max_ctx : 1;
+  if (kvc_decode_mma_scratch(pool, a->batch, r, max_ctx) > pool->scratch_bytes) return KVC_ERR_UNSUPPORTED;
+  Params P;
+  P.p = *pool;
+  P.rows = a->seq_rows;
+  P.batch = a->batch;
+  P.layer = a->layer;
+  P.r = r;
+  P.q = reinterpret_cast<const uint16_t *>(a->q);
+  P.k_new = reinterpret_cast<const uint16_t *>(a->k_new);
+  P.v_new = reinterpret_cast<const uint16_t *>(a->v_new);
+  P.out = a->out;
+  P.out_f32 = a->out_f32;
+  P.rows_out = a->rows_out;
+  P.rows_stride = a->rows_stride;
+  P.metric_mode = a->metric_mode;
+  P.append_fresh = a->append_fresh;
+  P.max_ctx_pad = (max_ctx + kItemTok - 1) / kItemTok * kItemTok;
+  P.n_ck = P.max_ctx_pad / kItemTok;
+  P.n_items = P.n_ck * a->batch * H;
+  P.scale = 1.4426950408889634f / sqrtf((float)D);
+  char *base = reinterpret_cast<char *>(pool->scratch);
+  P.counter = reinterpret_cast<int *>(base);  // work-queue head, zeroed per launch
+  int64_t off = 256;
+  P.scores = reinterpret_cast<float *>(base + off);
+  off += (int64_t)a->batch * H * P.max_ctx_pad * r * 4;
+  P.part_ml = reinterpret_cast<float *>(base + off);
+  off += (int64_t)a->batch * H * P.n_ck * 2 * kHP * 4;
+  P.part_o = reinterpret_cast<float *>(base + off);
+  switch (D) {
+    case 64: return launch<64>(P, s);
+    case 128: return launch<128>(P, s);
+    default: return launch<256>(P, s);
+  }
+}

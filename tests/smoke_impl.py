@@ -32,7 +32,7 @@ def run_smoke():
     for i, s in enumerate(seqs):
         ref, _ = O.decode_step_layer(st, s, 0, q[i], kn[i], vn[i], "L2")
         err = float(np.abs(out[i].cpu().numpy() - ref).max())
-        assert err < 2e-3, err
+        assert err < 1e-2, err  # bf16 P in the P.V MMA
     dst = rig.to_oracle()
     assert np.allclose(dst.metric, st.metric, rtol=1e-3, atol=1e-6)
     print("smoke: decode parity ok")
