@@ -35,7 +35,7 @@ constexpr int kNW = 4;           // warps per CTA
 constexpr int kThreads = kNW * 32;
 constexpr int kBlk = 16;         // tokens per KV block
 constexpr int kHP = 8;           // heads per MMA (group padded to 8)
-constexpr int kItemBlocks = 32;  // blocks per work item (512 positions)
+constexpr int kItemBlocks = 16;  // blocks per (warp) work item: 256 positions
 constexpr int kItemTok = kItemBlocks * kBlk;
 
 struct Params {
@@ -105,108 +105,103 @@ __device__ __forceinline__ uint32_t swz(int row, int c) {
   return (uint32_t)((c >> 3) * (kBlk * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4));
 }
 
-// Item descriptor shared by the CTA's warps.
-struct Item {
-  int id;        // -1 = none
-  int bi, head;
-  int t0, t1;    // positions [t0, t1) of the head in this item
-  int c_old;     // context before the append
-  int hidx_lo;   // low 32 bits of the head index (tables)
+// Warp work item: (sequence, KV head, kItemTok positions) + its block ids.
+struct WItem {
+  int id;     // -1 = none
+  int bi, head, t0, t1, c_old, nblk;
+  int64_t hidx;
+  int32_t blk[kItemBlocks];
 };
 
-__device__ void decode_item(const Params &P, int id, Item &it) {
+// Lane 0 pulls item ids until a non-empty chunk (or the queue ends); the
+// whole warp then loads the item's table entries.  Chunk-major order keeps
+// the long heads' tail chunks at the end of the queue.
+__device__ void fetch_item(const Params &P, WItem &w, int lane) {
   const kvc_pool &p = P.p;
   const int H = p.num_kv_heads;
   const int pairs = P.batch * H;
-  it.id = -1;
-  while (id < P.n_items) {
-    const int ck = id / pairs, pair = id % pairs;
-    const int bi = pair / H, head = pair % H;
-    const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
-    const int c_old = p.ctx[hidx];
-    const int cp = c_old + (P.k_new ? 1 : 0);
-    const int t0 = ck * kItemTok;
-    if (t0 < cp && cp <= p.nblocks[hidx] * kBlk) {
-      it.id = id;
-      it.bi = bi;
-      it.head = head;
-      it.t0 = t0;
-      it.t1 = min(cp, t0 + kItemTok);
-      it.c_old = c_old;
-      it.hidx_lo = (int)hidx;
-      return;
+  int id = -1, bi = 0, head = 0, t0 = 0, t1 = 0, c_old = 0;
+  int64_t hidx = 0;
+  if (lane == 0) {
+    while (true) {
+      const int cand = atomicAdd(P.counter, 1);
+      if (cand >= P.n_items) break;
+      const int ck = cand / pairs, pair = cand % pairs;
+      const int b_ = pair / H, h_ = pair % H;
+      const int64_t hx = head_index(p, P.rows[b_], P.layer, h_);
+      const int co = p.ctx[hx];
+      const int cp = co + (P.k_new ? 1 : 0);
+      const int s0 = ck * kItemTok;
+      if (s0 < cp && cp <= p.nblocks[hx] * kBlk) {
+        id = cand; bi = b_; head = h_; t0 = s0; t1 = min(cp, s0 + kItemTok); c_old = co; hidx = hx;
+        break;
+      }
     }
-    return;  // empty chunk: caller fetches again
   }
+  id = __shfl_sync(0xffffffffu, id, 0);
+  if (id < 0) {
+    if (lane == 0) w.id = -1;
+    __syncwarp();
+    return;
+  }
+  bi = __shfl_sync(0xffffffffu, bi, 0);
+  head = __shfl_sync(0xffffffffu, head, 0);
+  t0 = __shfl_sync(0xffffffffu, t0, 0);
+  t1 = __shfl_sync(0xffffffffu, t1, 0);
+  c_old = __shfl_sync(0xffffffffu, c_old, 0);
+  hidx = __shfl_sync(0xffffffffu, hidx, 0);
+  const int nblk = (t1 - 1) / kBlk - t0 / kBlk + 1;
+  if (lane < nblk) w.blk[lane] = p.tables[hidx * p.max_blocks + t0 / kBlk + lane];
+  if (lane == 0) {
+    w.id = id; w.bi = bi; w.head = head; w.t0 = t0; w.t1 = t1; w.c_old = c_old; w.nblk = nblk; w.hidx = hidx;
+  }
+  __syncwarp();
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2) k_decode_stream(const __grid_constant__ CUtensorMap tmK,
-                                                              const __grid_constant__ CUtensorMap tmV,
-                                                              const Params P) {
+__global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constant__ CUtensorMap tmK,
+                                                           const __grid_constant__ CUtensorMap tmV,
+                                                           const Params P) {
   constexpr int kBlkBytes = kBlk * D * 2;
   constexpr int kStageBytes = 2 * kBlkBytes;
   constexpr int kKS = D / 16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stages = P.stages;
-  uint8_t *ring = smem;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(ring + kNW * stages * kStageBytes);
-  float *wml = reinterpret_cast<float *>(bars + kNW * stages);  // [kNW][2][kHP]
-  float *wo = wml + kNW * 2 * kHP;                              // [kNW][kHP][D]
-  Item *items = reinterpret_cast<Item *>(wo + kNW * kHP * D);   // [2] current / next
   const kvc_pool &p = P.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int H = p.num_kv_heads, r = P.r, n_q = H * r;
   const bool append = P.k_new != nullptr;
+  uint8_t *my_ring = smem + warp * stages * kStageBytes;
+  uint64_t *my_bars = reinterpret_cast<uint64_t *>(smem + kNW * stages * kStageBytes) + warp * stages;
+  WItem *wit = reinterpret_cast<WItem *>(smem + kNW * stages * kStageBytes + kNW * stages * 8) + warp * 2;
 
-  uint8_t *my_ring = ring + warp * stages * kStageBytes;
-  uint64_t *my_bars = bars + warp * stages;
   if (lane == 0)
     for (int s = 0; s < stages; ++s) mbar_init(&my_bars[s], 1);
   fence_barrier_init();
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
-    // fetch the first two non-empty items
-    for (int k = 0; k < 2; ++k) {
-      Item it;
-      it.id = -1;
-      while (true) {
-        const int id = atomicAdd(P.counter, 1);
-        if (id >= P.n_items) break;
-        decode_item(P, id, it);
-        if (it.id >= 0) break;
-      }
-      items[k] = it;
-    }
   }
-  __syncthreads();
+  __syncwarp();
   const uint64_t pol = policy_evict_first();
-  const int32_t *tables = p.tables;
+  fetch_item(P, wit[0], lane);
+  fetch_item(P, wit[1], lane);
 
-  // Per-warp block stream over (current item, next item): blocks w, w+kNW, ...
-  // of each item.  `issued` counts ring fills, `done` ring drains.
-  int cur = 0;  // items[cur] is the item being computed
-  int issue_item = 0, issue_k = 0;  // next block to issue: items[(cur+issue_item)&1], k-th of this warp
+  // the warp's block stream: all blocks of wit[cur], then of wit[cur^1]
+  int cur = 0;
+  int iss_item = 0, iss_k = 0;  // next fill: block iss_k of wit[(cur+iss_item)&1]
   int issued = 0, done = 0;
-  auto my_nblocks = [&](const Item &it) {
-    if (it.id < 0) return 0;
-    const int nblk = (it.t1 - 1) / kBlk - it.t0 / kBlk + 1;
-    return nblk > warp ? (nblk - warp + kNW - 1) / kNW : 0;
-  };
-  auto try_issue = [&]() {
-    // lane 0 only: keep `stages` fills ahead across the two visible items
-    while (issued - done < stages && issue_item < 2) {
-      const Item &it = items[(cur + issue_item) & 1];
-      const int nb = my_nblocks(it);
-      if (issue_k >= nb) {
-        if (issue_item == 0 && it.id >= 0) { issue_item = 1; issue_k = 0; continue; }
+  auto try_issue = [&]() {  // lane 0
+    while (issued - done < stages && iss_item < 2) {
+      const WItem &w = wit[(cur + iss_item) & 1];
+      if (w.id < 0) break;
+      if (iss_k >= w.nblk) {
+        if (iss_item == 0) { iss_item = 1; iss_k = 0; continue; }
         break;
       }
-      const int blk = it.t0 / kBlk + warp + issue_k * kNW;
-      const int y = tables[(int64_t)it.hidx_lo * p.max_blocks + blk] * kBlk;
+      const int y = w.blk[iss_k] * kBlk;
       const int s = issued % stages;
       uint8_t *dst = my_ring + s * kStageBytes;
       fence_proxy_async();
@@ -214,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_decode_stream(const __grid_cons
       tma3d(dst, &tmK, 0, y, 0, &my_bars[s], pol);
       tma3d(dst + kBlkBytes, &tmV, 0, y, 0, &my_bars[s], pol);
       ++issued;
-      ++issue_k;
+      ++iss_k;
     }
   };
   if (lane == 0) try_issue();
@@ -225,14 +220,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_decode_stream(const __grid_cons
   const int lt_cadd = (lane >> 3) & 1;
   const bool hv0 = 2 * t < r, hv1 = 2 * t + 1 < r;
 
-  while (items[cur].id >= 0) {
-    const Item it = items[cur];
-    const int pair = it.bi * H + it.head;
-    // Q^T B-fragments of this item's query group
+  while (wit[cur].id >= 0) {
+    const int bi = wit[cur].bi, head = wit[cur].head, t0 = wit[cur].t0, t1 = wit[cur].t1;
+    const int c_old = wit[cur].c_old, nblk = wit[cur].nblk, item_id = wit[cur].id;
+    const int pair = bi * H + head;
     uint32_t qb[kKS][2];
     {
       const bool real = g < r;
-      const uint16_t *qrow = P.q + ((int64_t)it.bi * n_q + it.head * r + (real ? g : 0)) * D;
+      const uint16_t *qrow = P.q + ((int64_t)bi * n_q + head * r + (real ? g : 0)) * D;
 #pragma unroll
       for (int kk = 0; kk < kKS; ++kk) {
         qb[kk][0] = real ? *reinterpret_cast<const uint32_t *>(qrow + kk * 16 + 2 * t) : 0u;
@@ -244,20 +239,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_decode_stream(const __grid_cons
 #pragma unroll
     for (int i = 0; i < kKS; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
     float *srow_base = P.scores + (int64_t)pair * P.max_ctx_pad * r;
-    const int nb_me = my_nblocks(it);
-    for (int k = 0; k < nb_me; ++k) {
+    for (int k = 0; k < nblk; ++k) {
       const int s = done % stages;
       mbar_wait(&my_bars[s], (done / stages) & 1);
       uint8_t *kb = my_ring + s * kStageBytes;
       uint8_t *vb = kb + kBlkBytes;
-      const int blk = it.t0 / kBlk + warp + k * kNW;
-      const int tb0 = blk * kBlk;
-      const int valid = min(kBlk, it.t1 - tb0);
-      if (append && it.c_old >= tb0 && it.c_old < tb0 + kBlk) {
-        const int off = it.c_old - tb0;
-        const int64_t slot = (int64_t)tables[(int64_t)it.hidx_lo * p.max_blocks + blk] * kBlk + off;
-        const uint4 *kn = reinterpret_cast<const uint4 *>(P.k_new + ((int64_t)it.bi * H + it.head) * D);
-        const uint4 *vn = reinterpret_cast<const uint4 *>(P.v_new + ((int64_t)it.bi * H + it.head) * D);
+      const int tb0 = (t0 / kBlk + k) * kBlk;
+      const int valid = min(kBlk, t1 - tb0);
+      if (append && c_old >= tb0 && c_old < tb0 + kBlk) {
+        const int off = c_old - tb0;
+        const int64_t slot = (int64_t)wit[cur].blk[k] * kBlk + off;
+        const uint4 *kn = reinterpret_cast<const uint4 *>(P.k_new + ((int64_t)bi * H + head) * D);
+        const uint4 *vn = reinterpret_cast<const uint4 *>(P.v_new + ((int64_t)bi * H + head) * D);
         for (int c = lane; c < D / 8; c += 32) {
           const uint4 kv = kn[c], vv = vn[c];
           *reinterpret_cast<uint4 *>(kb + swz(off, c)) = kv;
@@ -323,78 +316,42 @@ __global__ void __launch_bounds__(kThreads, 2) k_decode_stream(const __grid_cons
       ++done;
       if (lane == 0) try_issue();
     }
-    // ---- merge the warps' (m, l, O) into this item's partial ----
+    // ---- this item's partial (m, l, O) straight from registers ----
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
       l0 += __shfl_xor_sync(0xffffffffu, l0, o);
       l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
+    const int ck = t0 / kItemTok;
+    float *pml = P.part_ml + ((int64_t)pair * P.n_ck + ck) * 2 * kHP;
+    float *po = P.part_o + ((int64_t)pair * P.n_ck + ck) * r * D;
     if (g == 0) {
-      wml[(warp * 2) * kHP + 2 * t] = m0;
-      wml[(warp * 2) * kHP + 2 * t + 1] = m1;
-      wml[(warp * 2 + 1) * kHP + 2 * t] = l0;
-      wml[(warp * 2 + 1) * kHP + 2 * t + 1] = l1;
+      pml[2 * t] = m0;
+      pml[2 * t + 1] = m1;
+      pml[kHP + 2 * t] = l0;
+      pml[kHP + 2 * t + 1] = l1;
     }
 #pragma unroll
     for (int mt = 0; mt < kKS; ++mt) {
-      float *w0 = wo + (warp * kHP + 2 * t) * D + mt * 16;
-      float *w1 = wo + (warp * kHP + 2 * t + 1) * D + mt * 16;
-      w0[g] = oacc[mt][0];
-      w1[g] = oacc[mt][1];
-      w0[g + 8] = oacc[mt][2];
-      w1[g + 8] = oacc[mt][3];
-    }
-    __syncthreads();
-    const int ck = it.t0 / kItemTok;
-    float *pml = P.part_ml + ((int64_t)pair * P.n_ck + ck) * 2 * kHP;
-    float *po = P.part_o + ((int64_t)pair * P.n_ck + ck) * r * D;
-    for (int e = threadIdx.x; e < r * D; e += kThreads) {
-      const int h = e / D;
-      float mx = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, wml[(w * 2) * kHP + h]);
-      float o = 0.f;
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) {
-        const float mw = wml[(w * 2) * kHP + h];
-        if (mw != -INFINITY) o += wo[(w * kHP + h) * D + (e % D)] * exp2f(mw - mx);
+      if (hv0) {
+        po[(2 * t) * D + mt * 16 + g] = oacc[mt][0];
+        po[(2 * t) * D + mt * 16 + g + 8] = oacc[mt][2];
       }
-      po[e] = o;
-    }
-    if (threadIdx.x < kHP) {
-      const int h = threadIdx.x;
-      float mx = -INFINITY, l = 0.f;
-      for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, wml[(w * 2) * kHP + h]);
-      for (int w = 0; w < kNW; ++w) {
-        const float mw = wml[(w * 2) * kHP + h];
-        if (mw != -INFINITY) l += wml[(w * 2 + 1) * kHP + h] * exp2f(mw - mx);
+      if (hv1) {
+        po[(2 * t + 1) * D + mt * 16 + g] = oacc[mt][1];
+        po[(2 * t + 1) * D + mt * 16 + g + 8] = oacc[mt][3];
       }
-      pml[h] = mx;
-      pml[kHP + h] = l;
     }
-    // advance: next item becomes current; fetch a new next
-    if (threadIdx.x == 0) {
-      Item nx;
-      nx.id = -1;
-      if (items[cur ^ 1].id >= 0) {
-        while (true) {
-          const int id = atomicAdd(P.counter, 1);
-          if (id >= P.n_items) break;
-          decode_item(P, id, nx);
-          if (nx.id >= 0) break;
-        }
-      }
-      items[cur] = nx;  // slot of the finished item now holds the one after next
-    }
-    __syncthreads();
+    (void)item_id;
+    // advance: the fetched-ahead item becomes current; refill the other slot
+    const int fin = cur;
     cur ^= 1;
-    // the issue window moves with `cur`
-    if (issue_item == 1) {
-      issue_item = 0;
-    } else {
-      issue_item = 0;
-      issue_k = 0;
-    }
+    if (iss_item == 1) iss_item = 0;
+    else { iss_item = 0; iss_k = 0; }
+    __syncwarp();
+    if (wit[cur].id >= 0) fetch_item(P, wit[fin], lane);
+    else if (lane == 0) wit[fin].id = -1;
+    __syncwarp();
     if (lane == 0) try_issue();
   }
 }
@@ -533,8 +490,7 @@ static bool pool_map(CUtensorMap *out, const void *base, int64_t rows, int D) {
 }
 
 int stream_smem(int D, int stages) {
-  return kNW * stages * 2 * kBlk * D * 2 + kNW * stages * 8 + kNW * 2 * kHP * 4 + kNW * kHP * D * 4 +
-         2 * (int)sizeof(Item) + 1024 + 64;
+  return kNW * stages * 2 * kBlk * D * 2 + kNW * stages * 8 + kNW * 2 * (int)sizeof(WItem) + 1024 + 64;
 }
 
 template <int D>
