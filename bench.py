@@ -161,27 +161,26 @@ def eviction_rounds(S, args):
     for s in range(args.prefill_seqs):
         manager.allocate_prefill(s, L)
         q = torch.randn((l, S["n_q"], 8, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-        k2_t, sc_t = 0.0, 0.0
+        k = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        v = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        e0, e1, e2 = ev(), ev(), ev()
+        torch.cuda.synchronize()
+        e0.record()
         for m in range(l):
-            k = torch.randn((H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-            v = torch.randn((H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-            e0, e1, e2 = ev(), ev(), ev()
-            e0.record()
-            K.prefill.write_prefill_kv(cache, tables, s, m, k, v)
-            e1.record()
-            p = K.cache.pool_struct(cache=cache, tables=tables, store=store)
-            K.prefill._window_call(q[m], k, S["mcfg"], H, d, dev, pool_p=p, seq_row=tables.row(s), layer=m)
-            e2.record()
-            torch.cuda.synchronize()
-            sc_t += e0.elapsed_time(e1)
-            k2_t += e1.elapsed_time(e2)
+            K.prefill.write_prefill_kv(cache, tables, s, m, k[m], v[m])
+        e1.record()
+        p = K.cache.pool_struct(cache=cache, tables=tables, store=store)
+        K.prefill._window_call(q, k, S["mcfg"], H, d, dev, pool_p=p, seq_row=tables.row(s), layer=0)
+        e2.record()
+        torch.cuda.synchronize()
+        sc_t = e0.elapsed_time(e1)
+        k2_t = e1.elapsed_time(e2)
+        del k, v
         S["_lib"].DeviceContext.get(dev).raise_status()
         E = K.budget_to_blocks(S["keep_tokens"], l, H, b, tables.sequence_block_count(s))
         e0, e1 = ev(), ev()
         torch.cuda.synchronize()
-        e0.record()
-        plan = K.compress(cache, tables, manager, store, {s: E}, sync=False)
-        e1.record()
+        plan = K.compress(cache, tables, manager, store, {s: E}, sync=False, events=(e0, e1))
         torch.cuda.synchronize()
         S["_lib"].DeviceContext.get(dev).raise_status()
         tot = plan.totals.tolist()

@@ -206,6 +206,12 @@ typedef struct kvc_window_args {
   int32_t aggregation;      /* 1 L1, 2 L2 */
   int32_t protect_window;
   float *metrics_out;       /* NULL or f32 [heads][L] pooled metrics */
+  /* several consecutive layers in one call (layer, layer+1, ...): strides in
+   * elements between the layers' q_win / k / metrics_out; n_layers <= 1 = one */
+  int32_t n_layers;
+  int64_t q_layer_stride;
+  int64_t k_layer_stride;
+  int64_t out_layer_stride;
 } kvc_window_args;
 
 int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *args, void *stream);

@@ -62,7 +62,8 @@ class WindowArgs(ctypes.Structure):
     _fields_ = [
         ("seq_row", _i32), ("layer", _i32), ("num_query_heads", _i32), ("L", _i32),
         ("q_win", _p), ("k", _p), ("window", _i32), ("pool", _i32), ("aggregation", _i32),
-        ("protect_window", _i32), ("metrics_out", _p),
+        ("protect_window", _i32), ("metrics_out", _p), ("n_layers", _i32), ("q_layer_stride", _i64),
+        ("k_layer_stride", _i64), ("out_layer_stride", _i64),
     ]
 
 

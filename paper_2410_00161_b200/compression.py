@@ -204,7 +204,7 @@ def _args(plan: EvictionPlan) -> _lib.EvictArgs:
 def _scratch_bytes(plan: EvictionPlan, hp: int) -> int:
     n = len(plan.seq_ids)
     T = n * hp
-    return T * plan.max_slots * 4 + T * 12 + n * (2048 * 4 + 32) + (1 << 16)
+    return T * ((plan.max_slots + 3) // 4 * 4) * 4 + T * 12 + n * (2048 * 4 + 32) + (1 << 16)
 
 
 def schedule_evictions(tables: BlockTables, store: MetricsStore, budgets: Mapping[int, int],
@@ -261,16 +261,21 @@ def refresh_ctx_bounds(tables: BlockTables, seq_ids) -> None:
 
 
 def compress(cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
-             budgets: Mapping[int, int], sync: bool = True, record_moves: bool = True):
+             budgets: Mapping[int, int], sync: bool = True, record_moves: bool = True, events=None):
     """Run the full eviction pipeline for a batch of per-sequence budgets
-    (compression.py:312-355): one scheduling + compaction pass on the GPU."""
+    (compression.py:312-355): one scheduling + compaction pass on the GPU.
+    `events` = (start, end) CUDA events recorded around the device work."""
     plan = _prepare(tables, budgets, want_moves=True, want_freed=True)
     if plan.seq_ids:
         hp = tables.num_layers * tables.num_kv_heads
         p = with_scratch(pool_struct(cache=cache, tables=tables, manager=manager, store=store), tables.device,
                          _scratch_bytes(plan, hp))
         a = _args(plan)
+        if events:
+            events[0].record()
         _lib.check(_lib.lib().kvc_compress(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(tables.device)),
                    "compress")
+        if events:
+            events[1].record()
         plan.executed = True
     return _finish(tables, plan, sync, record_moves)

@@ -129,18 +129,55 @@ __global__ void __launch_bounds__(kThreads) k_load(kvc_pool p, const int32_t *ro
   if (threadIdx.x == 0) shield_s = 0;
   __syncthreads();
   int shield = 0;
-  for (int64_t base = 0; base < n; base += kThreads) {
-    const int64_t pos = base + threadIdx.x;
-    const bool in = pos < n;
-    uint32_t key = 0;
-    if (in) {
-      const int64_t f = (int64_t)tab[pos / b] * b + pos % b;
-      const bool occ = pos < C;
-      key = slot_key(p, f, occ);
-      shield += (occ && (p.protected_[f] | p.fresh[f])) ? 1 : 0;
-      keys[pos] = key;
+  if (b == 16) {
+    // one thread per 16-slot block: 64 B metric, 16 B flags, 64 B keys
+    for (int64_t base = 0; base < nb; base += kThreads) {
+      const int64_t bl = base + threadIdx.x;
+      const bool in = bl < nb;
+      uint32_t kk[16];
+      if (in) {
+        const int64_t f0 = (int64_t)tab[bl] * 16;
+        const float4 *mp = reinterpret_cast<const float4 *>(p.metric + f0);
+        const uint4 pr = *reinterpret_cast<const uint4 *>(p.protected_ + f0);
+        const uint4 fr = *reinterpret_cast<const uint4 *>(p.fresh + f0);
+        const uint32_t pw[4] = {pr.x | fr.x, pr.y | fr.y, pr.z | fr.z, pr.w | fr.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 mv = mp[q];
+          const float mf[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int o = q * 4 + e;
+            const int64_t pos = bl * 16 + o;
+            const bool occ = pos < C;
+            const bool sh = occ && ((pw[q] >> (8 * e)) & 0xff);
+            shield += sh ? 1 : 0;
+            kk[o] = !occ ? f32_order_key(0.f) : sh ? kKeyInf : f32_order_key(mf[e]);
+          }
+        }
+        uint4 *kp = reinterpret_cast<uint4 *>(keys + bl * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kp[q] = make_uint4(kk[4 * q], kk[4 * q + 1], kk[4 * q + 2], kk[4 * q + 3]);
+      }
+      if (with_hist) {
+#pragma unroll
+        for (int o = 0; o < 16; ++o) hist_add(hist, in ? kk[o] >> 21 : 0, in);
+      }
     }
-    if (with_hist) hist_add(hist, key >> 21, in);
+  } else {
+    for (int64_t base = 0; base < n; base += kThreads) {
+      const int64_t pos = base + threadIdx.x;
+      const bool in = pos < n;
+      uint32_t key = 0;
+      if (in) {
+        const int64_t f = (int64_t)tab[pos / b] * b + pos % b;
+        const bool occ = pos < C;
+        key = slot_key(p, f, occ);
+        shield += (occ && (p.protected_[f] | p.fresh[f])) ? 1 : 0;
+        keys[pos] = key;
+      }
+      if (with_hist) hist_add(hist, key >> 21, in);
+    }
   }
   atomicAdd(&shield_s, shield);
   __syncthreads();
@@ -233,13 +270,18 @@ __global__ void __launch_bounds__(kThreads) k_hist(kvc_pool p, const int32_t *ro
   if (threadIdx.x == 0) below_s = 0;
   __syncthreads();
   int32_t below = 0;
-  for (int64_t base = 0; base < n; base += kThreads) {
-    const int64_t pos = base + threadIdx.x;
-    uint32_t key = pos < n ? keys[pos] : 0xffffffffu;
-    const uint32_t top = key >> shift_hi;
-    const bool match = pos < n && top == pre;
-    below += (pos < n && top < pre) ? 1 : 0;
-    hist_add(hist, (key >> shift) & dmask, match);
+  for (int64_t base = 0; base < n; base += 4 * kThreads) {
+    const int64_t pos = base + 4 * threadIdx.x;  // max_slots is a multiple of 4
+    uint4 k4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    if (pos < n) k4 = *reinterpret_cast<const uint4 *>(keys + pos);
+    const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool in = pos + e < n;
+      const uint32_t top = kv[e] >> shift_hi;
+      below += (in && top < pre) ? 1 : 0;
+      hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
+    }
   }
   atomicAdd((unsigned long long *)&below_s, (unsigned long long)below);
   __syncthreads();
@@ -483,7 +525,8 @@ __global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t 
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
     return;
   }
-  // concurrent moves: small fields per thread, K/V rows per warp (16 B lanes)
+  // the metric/logical/flag moves happen here (renumbering below needs them);
+  // the K/V rows move in k_copy_kv, a bandwidth kernel over all move lists
   for (int k = threadIdx.x; k < nmoves; k += kThreads) {
     const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
     p.metric[dst] = p.metric[src];
@@ -491,30 +534,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t 
     p.protected_[dst] = p.protected_[src];
     p.fresh[dst] = p.fresh[src];
   }
-  if (D % 8 != 0) {  // small head_dim: element copies
-    uint16_t *kc = reinterpret_cast<uint16_t *>(p.k_cache);
-    uint16_t *vc = reinterpret_cast<uint16_t *>(p.v_cache);
-    const int64_t total = (int64_t)nmoves * D;
-    for (int64_t i = threadIdx.x; i < total; i += kThreads) {
-      const int64_t k = i / D, c = i % D;
-      const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
-      kc[dst * D + c] = kc[src * D + c];
-      vc[dst * D + c] = vc[src * D + c];
-    }
-  } else {
-    const int vec = D / 8;  // 16-byte chunks per row
-    uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
-    uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
-    const int64_t total = (int64_t)nmoves * vec;
-    for (int64_t i = threadIdx.x; i < total; i += kThreads) {
-      const int64_t k = i / vec, c = i % vec;
-      const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
-      const uint4 kv = kc[src * vec + c];
-      const uint4 vv = vc[src * vec + c];
-      kc[dst * vec + c] = kv;
-      vc[dst * vec + c] = vv;
-    }
-  }
+  (void)D;
   __syncthreads();
   // free the trailing e blocks, reset their slots
   for (int64_t i = threadIdx.x; i < (int64_t)e * b; i += kThreads) {
@@ -582,6 +602,79 @@ __global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t 
   }
 }
 
+// K/V rows of every move of the round: grid (head, part); a warp moves one
+// (K, V) row pair per step with 16-byte lanes, 4 pairs in flight per warp.
+// Sources are inside blocks freed by k_compact; nothing can reuse them before
+// this kernel completes (stream order).
+__global__ void __launch_bounds__(256) k_copy_kv(kvc_pool p, const int32_t *moves, const int64_t *move_off,
+                                                const int32_t *move_counts) {
+  const int g = blockIdx.x;
+  const int n = move_counts[g];
+  if (n == 0) return;
+  const int D = p.head_dim;
+  const int32_t *mv = moves + move_off[g] * 2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nwarps = blockDim.x / 32 * gridDim.y;
+  const int wid = blockIdx.y * (blockDim.x / 32) + warp;
+  if (D % 8 == 0 && D <= 256) {
+    const int vec = D / 8;  // 16-byte chunks per row (16 for d=128)
+    uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
+    uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
+    // each lane covers chunk (lane % vec) of K (lane < 16) or V rows
+    const int per = 32 / (2 * vec) > 0 ? 32 / (2 * vec) : 1;  // moves per warp step
+    for (int base = wid * per * 4; base < n; base += nwarps * per * 4) {
+      uint4 val[4];
+      int64_t dst[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int slot_lane = lane / (2 * vec);
+        const int k = base + u * per + slot_lane;
+        const int sub = lane % (2 * vec);
+        const bool isv = sub >= vec;
+        const int c = isv ? sub - vec : sub;
+        ok[u] = k < n && slot_lane < per;
+        if (ok[u]) {
+          const int64_t src = mv[2 * k];
+          dst[u] = (int64_t)mv[2 * k + 1] * vec + c;
+          val[u] = isv ? vc[src * vec + c] : kc[src * vec + c];
+          if (isv) dst[u] = -1 - dst[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!ok[u]) continue;
+        if (dst[u] >= 0) kc[dst[u]] = val[u];
+        else vc[-1 - dst[u]] = val[u];
+      }
+      if (2 * vec > 32) {  // d = 256: second half of the row
+        for (int u = 0; u < 4; ++u) {
+          const int k = base + u * per;
+          if (k >= n) continue;
+          const int64_t src = mv[2 * k], d0 = mv[2 * k + 1];
+          for (int c = lane; c < 2 * vec; c += 32) {
+            if (c < 32) continue;
+            const bool isv = c >= vec;
+            const int cc = isv ? c - vec : c;
+            if (isv) vc[d0 * vec + cc] = vc[src * vec + cc];
+            else kc[d0 * vec + cc] = kc[src * vec + cc];
+          }
+        }
+      }
+    }
+  } else {  // small or odd head_dim: element copies
+    uint16_t *kc = reinterpret_cast<uint16_t *>(p.k_cache);
+    uint16_t *vc = reinterpret_cast<uint16_t *>(p.v_cache);
+    const int64_t total = (int64_t)n * D;
+    for (int64_t i = (int64_t)wid * 32 + lane; i < total; i += (int64_t)nwarps * 32) {
+      const int64_t k = i / D, c = i % D;
+      const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
+      kc[dst * D + c] = kc[src * D + c];
+      vc[dst * D + c] = vc[src * D + c];
+    }
+  }
+}
+
 __global__ void k_free_total(kvc_pool p, int64_t *totals) {
   using Red = cub::BlockReduce<int64_t, 1024>;
   __shared__ typename Red::TempStorage tmp;
@@ -593,7 +686,7 @@ __global__ void k_free_total(kvc_pool p, int64_t *totals) {
 
 int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, EvictState &S) {
   S.hp = pool->num_layers * pool->num_kv_heads;
-  S.max_slots = a->max_slots_per_head;
+  S.max_slots = (a->max_slots_per_head + 3) & ~int64_t(3);  // uint4 key rows
   S.status = pool->status;
   const int64_t T = (int64_t)a->n_seqs * S.hp;
   S.keys = sc.take<uint32_t>(T * S.max_slots);
@@ -643,6 +736,7 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
   }
   if (dyn > 200 * 1024) return KVC_ERR_UNSUPPORTED;
   k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
+  if (pool->k_cache) k_copy_kv<<<dim3((unsigned)T, 8), 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts);
   if (a->totals) k_free_total<<<1, 1024, 0, s>>>(*pool, a->totals);
   KVC_CHECK_LAUNCH();
   return KVC_OK;

@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *ktiles = smem;                                  // kStages x kTileBytes
   uint8_t *qbuf = smem + kStages * kTileBytes;             // kQBytes
-  float *sbuf = reinterpret_cast<float *>(qbuf + kQBytes);  // pass 0: [128][N+1]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sbuf + kTileKeys * (N + 1));
+  int *lim_s = reinterpret_cast<int *>(qbuf + kQBytes);  // [N] last visible key per column (-1: pad)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(lim_s + N);
   uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2, *qfull = tempty + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qfull + 1);
   float *stat_s = reinterpret_cast<float *>(tmem_slot + 4);  // pass 1: M[N], invZ[N]
@@ -138,11 +138,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (PASS == 1) {
-    for (int c = threadIdx.x; c < N; c += kThreads) {
+  for (int c = threadIdx.x; c < N; c += kThreads) {
+    const bool real = c < P.RW;
+    lim_s[c] = real ? P.start + c % P.wq : -1;
+    if (PASS == 1) {
       const float2 st = P.stat[(int64_t)head * N + c];
-      stat_s[c] = st.x;
-      stat_s[N + c] = st.y;
+      stat_s[c] = real ? st.x : INFINITY;  // padded columns contribute exp2(-inf) * 0
+      stat_s[N + c] = real ? st.y : 0.f;
     }
   }
   tc_fence_before();
@@ -195,11 +197,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
     const int key_local = quad * 32 + lane;
-    float m_run = -INFINITY, z_run = 0.f;  // pass 0: this thread's (column, part)
-    constexpr int kParts = 128 / N;        // threads per column
-    const int col = et % N, part = et / N;
-    float raw_part = 0.f;
-    (void)raw_part;
+    // pass 0: per-thread online (max, sum exp2) of every column over this
+    // thread's keys; pass 1: M and 1/Z per column from the combine kernel.
+    float m[N], z[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      m[c] = PASS == 0 ? -INFINITY : stat_s[c];
+      z[c] = PASS == 0 ? 0.f : stat_s[N + c];
+    }
     for (int i = 0; i < ntiles; ++i) {
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i / 2) & 1);
@@ -209,56 +214,70 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int g = 0; g < N / 32; ++g) tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * N + g * 32, v + g * 32);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);  // 128 arrivals release the accumulator
-      const int j = (t_lo + i) * kTileKeys + key_local;  // key position within the head
+      const int tile0 = (t_lo + i) * kTileKeys;
+      const int j = tile0 + key_local;  // key position within the head
+      // every window row sees every key of this tile and the tile is inside L
+      const bool fast = tile0 + kTileKeys - 1 <= P.start && tile0 + kTileKeys <= P.L;
       if (PASS == 0) {
-        float *srow = sbuf + key_local * (N + 1);
+        if (fast) {
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-          const int ii = c % P.wq;
-          const bool ok = c < P.RW && j < P.L && j <= P.start + ii;
-          srow[c] = ok ? v[c] * P.scale : -INFINITY;
-        }
-        named_sync(1, 128);
-        // column `col`, keys part*(128/kParts) .. : online max / sum
-        constexpr int kSpan = 128 / kParts;
-        for (int k = 0; k < kSpan; ++k) {
-          const float s = sbuf[(part * kSpan + k) * (N + 1) + col];
-          if (s > m_run) {
-            z_run = z_run * exp2f(m_run - s) + 1.f;
-            m_run = s;
-          } else if (s > -INFINITY) {
-            z_run += exp2f(s - m_run);
+          for (int c = 0; c < N; ++c) {
+            const float s = v[c] * P.scale;
+            const float mn = fmaxf(m[c], s);
+            z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
+            m[c] = mn;
+          }
+        } else if (j < P.L) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) {
+            if (j <= lim_s[c]) {
+              const float s = v[c] * P.scale;
+              const float mn = fmaxf(m[c], s);
+              z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
+              m[c] = mn;
+            }
           }
         }
-        named_sync(1, 128);
       } else {
         float contrib = 0.f;
+        if (fast) {
 #pragma unroll
-        for (int c = 0; c < N; ++c) {
-          const int ii = c % P.wq;
-          const bool ok = c < P.RW && j <= P.start + ii;
-          const float pr = exp2f(v[c] * P.scale - stat_s[c]) * stat_s[N + c];
-          const float f = P.agg == 2 ? pr * pr : pr;
-          contrib += ok ? f : 0.f;
+          for (int c = 0; c < N; ++c) {
+            const float pr = exp2f(v[c] * P.scale - m[c]) * z[c];  // columns >= RW: M=+inf, 1/Z=0
+            contrib += P.agg == 2 ? pr * pr : pr;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < N; ++c) {
+            const float pr = exp2f(v[c] * P.scale - m[c]) * z[c];
+            const float f = P.agg == 2 ? pr * pr : pr;
+            contrib += j <= lim_s[c] ? f : 0.f;
+          }
         }
         if (j < P.L) P.raw[(int64_t)head * P.L + j] = contrib;
       }
     }
     if (PASS == 0) {
-      // combine the kParts partial (m, z) of each column
-      float2 *red = reinterpret_cast<float2 *>(sbuf);
-      red[et] = make_float2(m_run, z_run);
+      // combine the 128 threads' (m, z) per column through the (now idle) ring
+      named_sync(1, 128);
+      float *rm = reinterpret_cast<float *>(ktiles);
+      float *rz = rm + 128 * (N + 1);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        rm[et * (N + 1) + c] = m[c];
+        rz[et * (N + 1) + c] = z[c];
+      }
       named_sync(1, 128);
       if (et < N) {
-        float m = -INFINITY, z = 0.f;
-        for (int p2 = 0; p2 < kParts; ++p2) {
-          const float2 q = red[p2 * N + et];
-          if (q.x == -INFINITY) continue;
-          const float mn = fmaxf(m, q.x);
-          z = (m == -INFINITY ? 0.f : z * exp2f(m - mn)) + q.y * exp2f(q.x - mn);
-          m = mn;
+        float mm = -INFINITY, zz = 0.f;
+        for (int k = 0; k < 128; ++k) {
+          const float qm = rm[k * (N + 1) + et], qz = rz[k * (N + 1) + et];
+          if (qm == -INFINITY) continue;
+          const float mn = fmaxf(mm, qm);
+          zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + qz * exp2f(qm - mn);
+          mm = mn;
         }
-        P.partial[((int64_t)head * P.chunks + chunk) * N + et] = make_float2(m, z);
+        P.partial[((int64_t)head * P.chunks + chunk) * N + et] = make_float2(mm, zz);
       }
     }
   }
@@ -339,7 +358,7 @@ int run_window(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cud
   CUtensorMap tmK, tmQ;
   if (!make_map(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
   if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
-  const int smem = stages_for<D>() * kTileKeys * D * 2 + N * D * 2 + kTileKeys * (N + 1) * 4 + 256 + 2 * N * 4 + 1024;
+  const int smem = stages_for<D>() * kTileKeys * D * 2 + N * D * 2 + N * 4 + 256 + 2 * N * 4 + 1024;
   auto k0 = k_window<N, D, 0>;
   auto k1 = k_window<N, D, 1>;
   static bool configured = false;
@@ -379,7 +398,7 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   P.D = D;
   P.start = a->L - P.wq;
   P.tiles_per_head = (a->L + kTileKeys - 1) / kTileKeys;
-  int chunks = (148 + H - 1) / H;
+  int chunks = 148 / H > 0 ? 148 / H : 1;  // one wave: 1 CTA per SM
   if (chunks > P.tiles_per_head) chunks = P.tiles_per_head;
   P.chunks = chunks;
   P.scale = 1.4426950408889634f / sqrtf((float)D);
@@ -392,10 +411,23 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   P.raw = sc.take<float>((int64_t)H * a->L);
   if (!P.partial || !P.stat || !P.raw) return KVC_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  if (N == 32 && D == 64) return run_window<32, 64>(pool, a, P, s);
-  if (N == 32 && D == 128) return run_window<32, 128>(pool, a, P, s);
-  if (N == 32 && D == 256) return run_window<32, 256>(pool, a, P, s);
-  if (N == 64 && D == 64) return run_window<64, 64>(pool, a, P, s);
-  if (N == 64 && D == 128) return run_window<64, 128>(pool, a, P, s);
-  return KVC_ERR_UNSUPPORTED;
+  const int nl = a->n_layers > 1 ? a->n_layers : 1;
+  if (a->layer < 0 || (a->seq_row >= 0 && a->layer + nl > pool->num_layers)) return KVC_ERR_INVALID;
+  // one layer at a time: the layer's K (64 MB at Llama-8B shapes) stays in L2
+  // between the statistics pass and the metric pass
+  for (int li = 0; li < nl; ++li) {
+    kvc_window_args al = *a;
+    al.layer = a->layer + li;
+    al.q_win = reinterpret_cast<const uint16_t *>(a->q_win) + li * a->q_layer_stride;
+    al.k = reinterpret_cast<const uint16_t *>(a->k) + li * a->k_layer_stride;
+    al.metrics_out = a->metrics_out ? a->metrics_out + li * a->out_layer_stride : nullptr;
+    int rc = KVC_ERR_UNSUPPORTED;
+    if (N == 32 && D == 64) rc = run_window<32, 64>(pool, &al, P, s);
+    else if (N == 32 && D == 128) rc = run_window<32, 128>(pool, &al, P, s);
+    else if (N == 32 && D == 256) rc = run_window<32, 256>(pool, &al, P, s);
+    else if (N == 64 && D == 64) rc = run_window<64, 64>(pool, &al, P, s);
+    else if (N == 64 && D == 128) rc = run_window<64, 128>(pool, &al, P, s);
+    if (rc != KVC_OK) return rc;
+  }
+  return KVC_OK;
 }

@@ -33,12 +33,20 @@ def _dev_bf16(x, dev) -> torch.Tensor:
 
 def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev, pool_p=None,
                  seq_row: int = -1, layer: int = 0, metrics_out=None) -> None:
-    n_q, L = q.shape[0], k.shape[1]
+    """K2 for one layer (q (n_q, L|w', d), k (H, L, d)) or several consecutive
+    layers (q (l, n_q, L|w', d), k (l, H, L, d)) in one C call."""
+    multi = k.dim() == 4
+    if not multi:
+        q, k = q[None], k[None]
+        if metrics_out is not None:
+            metrics_out = metrics_out[None]
+    nl, n_q, L = k.shape[0], q.shape[1], k.shape[2]
     w = min(cfg.window, L)
-    q_win = q[:, L - w:, :] if q.shape[1] == L else q
-    if q_win.shape[1] != w:
-        raise ValueError(f"query window has {q_win.shape[1]} rows, expected {w}")
+    q_win = q[:, :, L - w:, :] if q.shape[2] == L else q
+    if q_win.shape[2] != w:
+        raise ValueError(f"query window has {q_win.shape[2]} rows, expected {w}")
     q_win = q_win.contiguous()
+    k = k.contiguous()
     a = _lib.WindowArgs()
     a.seq_row = seq_row
     a.layer = layer
@@ -51,6 +59,10 @@ def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev,
     a.aggregation = cfg.metric_mode
     a.protect_window = int(cfg.protect_window)
     a.metrics_out = _lib.ptr(metrics_out)
+    a.n_layers = nl
+    a.q_layer_stride = q_win[0].numel()
+    a.k_layer_stride = k[0].numel()
+    a.out_layer_stride = metrics_out[0].numel() if metrics_out is not None else 0
     if pool_p is None:
         pool_p = _lib.KvcPool()
         pool_p.status = _lib.DeviceContext.get(dev).status.data_ptr()
@@ -112,10 +124,18 @@ def prefill_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockM
     """Allocate + write + score a prompt: q (l, n_q, L or w, d), k/v (l, H, L, d).
 
     Raises PreemptionNeeded (nothing allocated) when the pool is short.
-    Returns the number of blocks allocated.
+    Returns the number of blocks allocated.  Asynchronous after allocation:
+    all layers' scatters, then one K2 call covering every layer.
     """
+    if cfg.mode != WINDOW:
+        raise ConfigError("mode", "the device prefill metric implements the observation window")
+    dev = cache.device
     L = k.shape[2]
     demand = manager.allocate_prefill(seq_id, L)
+    kt, vt, qt = _dev_bf16(k, dev), _dev_bf16(v, dev), _dev_bf16(q, dev)
     for layer in range(tables.num_layers):
-        prefill_layer(cache, tables, store, seq_id, layer, q[layer], k[layer], v[layer], cfg)
+        write_prefill_kv(cache, tables, seq_id, layer, kt[layer], vt[layer])
+    p = pool_struct(cache=cache, tables=tables, store=store)
+    _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
+                 seq_row=tables.row(seq_id), layer=0)
     return demand
