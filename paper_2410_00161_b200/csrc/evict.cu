@@ -44,6 +44,8 @@ struct EvictState {
   int32_t *cap;       // [T]
   int32_t *lo;        // [T] L_h
   int32_t *hi;        // [T] U_h
+  int32_t *ltc;       // [T] keys < T*
+  int32_t *lec;       // [T] keys <= T*
   // per sequence
   int32_t *R;         // [n_seqs][kBins] contribution deltas per digit
   uint32_t *prefix;   // [n_seqs] T* digits found so far
@@ -317,6 +319,8 @@ __global__ void __launch_bounds__(kThreads) k_bounds(kvc_pool p, const int32_t *
     const int cap = S.cap[g];
     S.lo[g] = lt / b < cap ? lt / b : cap;
     S.hi[g] = le / b < cap ? le / b : cap;
+    S.ltc[g] = lt;
+    S.lec[g] = le;
   }
 }
 
@@ -602,6 +606,331 @@ __global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_compact16: k_compact for block_size 16, 1024 threads, one thread per
+// 16-slot block in every pass (uint4 key / int4 logical rows).
+// ---------------------------------------------------------------------------
+
+constexpr int kT16 = 1024;
+
+__device__ void scan_hist16(int32_t *hist) {  // inclusive, kT16 threads
+  using Scan = cub::BlockScan<int32_t, kT16>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int per = kBins / kT16;
+  int32_t v[per];
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    v[i] = hist[threadIdx.x * per + i];
+    s += v[i];
+  }
+  int32_t excl;
+  __syncthreads();
+  Scan(tmp).ExclusiveSum(s, excl);
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    excl += v[i];
+    hist[threadIdx.x * per + i] = excl;
+  }
+  __syncthreads();
+}
+
+// rank-th smallest value among the positions `get4` marks valid, 4 per call.
+// Returns the value; *rank_out = its rank among equal values, *eq_out = how
+// many valid positions hold it.
+template <typename Get4>
+__device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, int64_t *rank_out,
+                             int64_t *eq_out) {
+  __shared__ uint32_t pre_s;
+  __shared__ int64_t rank_s, eq_s;
+  const int shifts[3] = {21, 10, 0};
+  const int bitsv[3] = {11, 11, 10};
+  uint32_t pre = 0;
+  int64_t eq = 0;
+  for (int lv = 0; lv < 3; ++lv) {
+    const int shift = shifts[lv], bits = bitsv[lv];
+    const int shift_hi = shift + bits;
+    const uint32_t dmask = (1u << bits) - 1;
+    for (int i = threadIdx.x; i < kBins; i += kT16) hist[i] = 0;
+    __syncthreads();
+    for (int64_t qb = 0; qb * 4 < n; qb += kT16) {  // warp-uniform trip count (hist_add votes)
+      const int64_t q = qb + threadIdx.x;
+      uint32_t v[4] = {0u, 0u, 0u, 0u};
+      bool ok[4] = {false, false, false, false};
+      if (q * 4 < n) get4(q * 4, v, ok);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool m = ok[e] && (shift_hi >= 32 || (v[e] >> shift_hi) == pre);
+        hist_add(hist, (v[e] >> shift) & dmask, m);
+      }
+    }
+    __syncthreads();
+    scan_hist16(hist);
+    for (int c = threadIdx.x; c < (1 << bits); c += kT16) {
+      const int64_t excl = c > 0 ? hist[c - 1] : 0;
+      if (excl <= rank && rank < hist[c]) {
+        pre_s = (pre << bits) | (uint32_t)c;
+        rank_s = rank - excl;
+        eq_s = hist[c] - excl;
+      }
+    }
+    __syncthreads();
+    pre = pre_s;
+    rank = rank_s;
+    eq = eq_s;
+    __syncthreads();
+  }
+  *rank_out = rank;
+  *eq_out = eq;
+  return pre;
+}
+
+__global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
+  extern __shared__ uint32_t bitmap[];  // [words] bitmap + [words] prefix
+  __shared__ int32_t hist[kBins];
+  __shared__ int32_t cnt_s[4];
+  using Scan = cub::BlockScan<int32_t, kT16>;
+  __shared__ typename Scan::TempStorage stmp;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  const int e = M.evict[g];
+  if (threadIdx.x == 0 && M.move_counts) M.move_counts[g] = 0;
+  if (threadIdx.x == 0 && M.evicted_kvs) M.evicted_kvs[g] = 0;
+  if (e <= 0) return;
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int nb = p.nblocks[hidx];
+  const int C = p.ctx[hidx];
+  const int64_t n = (int64_t)nb * 16;
+  int32_t *tab = head_table(p, hidx);
+  const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+
+  // ---- threshold T_h = (16 e)-th smallest key; shortcut when it is T* ----
+  const uint32_t Tstar = S.prefix[si];
+  const int64_t lt = S.ltc[g], le = S.lec[g];
+  const int64_t target = (int64_t)16 * e - 1;
+  uint32_t T;
+  int64_t tie_rank, tie_cnt;
+  if (target >= lt) {
+    T = Tstar;
+    tie_rank = target - lt;
+    tie_cnt = le - lt;
+  } else {
+    T = select16(hist, n, target, [&](int64_t pos, uint32_t *v, bool *ok) {
+      const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
+      v[0] = k4.x; v[1] = k4.y; v[2] = k4.z; v[3] = k4.w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ok[i] = pos + i < n && v[i] < Tstar;
+    }, &tie_rank, &tie_cnt);
+  }
+  // ---- tie cut: ties at T ordered by (occupied, logical, position) ----
+  auto sec = [&](int64_t pos, int32_t lg) -> uint32_t {
+    return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
+  };
+  uint32_t Sx = 0xffffffffu;
+  if (tie_rank + 1 < tie_cnt) {
+    int64_t dummy, dummy2;
+    Sx = select16(hist, n, tie_rank, [&](int64_t pos, uint32_t *v, bool *ok) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t ps = pos + i;
+        ok[i] = ps < n && keys[ps] == T;
+        v[i] = ok[i] ? sec(ps, p.logical[(int64_t)tab[ps / 16] * 16 + ps % 16]) : 0u;
+      }
+    }, &dummy, &dummy2);
+  }
+
+  // ---- MoveCache pairing (holes ascending below R0, survivors descending) ----
+  const int rb = nb - e;  // first block of the eviction range
+  int32_t *mv = M.moves + M.move_off[g] * 2;
+  const int64_t cap_mv = (int64_t)16 * e;
+  if (threadIdx.x == 0) { cnt_s[0] = 0; cnt_s[1] = 0; cnt_s[2] = 0; }
+  __syncthreads();
+  int32_t evk = 0;
+  auto block_flags = [&](int bl, uint32_t &masked_bits, uint32_t &live_bits) {
+    const int64_t f0 = (int64_t)tab[bl] * 16;
+    const uint4 *kp = reinterpret_cast<const uint4 *>(keys + (int64_t)bl * 16);
+    const int4 *lp = reinterpret_cast<const int4 *>(p.logical + f0);
+    masked_bits = 0;
+    live_bits = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 k4 = kp[q];
+      const int4 l4 = lp[q];
+      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int o = q * 4 + i;
+        const int64_t pos = (int64_t)bl * 16 + o;
+        const bool m = kv[i] < T || (kv[i] == T && (Sx == 0xffffffffu || sec(pos, lv[i]) <= Sx));
+        masked_bits |= (m ? 1u : 0u) << o;
+        live_bits |= (lv[i] >= 0 ? 1u : 0u) << o;
+      }
+    }
+  };
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < rb; base += kT16) {
+      const int bl = base + threadIdx.x;
+      uint32_t holes = 0;
+      int64_t f0 = 0;
+      if (bl < rb) {
+        uint32_t mb, lb;
+        block_flags(bl, mb, lb);
+        holes = mb | ~lb;
+        holes &= 0xffffu;
+        const int occ_n = C - bl * 16;
+        const uint32_t occ_bits = occ_n >= 16 ? 0xffffu : occ_n <= 0 ? 0u : ((1u << occ_n) - 1u);
+        evk += __popc(mb & occ_bits);
+        f0 = (int64_t)tab[bl] * 16;
+      }
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(__popc(holes), excl, tot);
+      int64_t k = carry + excl;
+      for (uint32_t hb = holes; hb; hb &= hb - 1) {
+        const int o = __ffs(hb) - 1;
+        if (k < cap_mv) mv[2 * k + 1] = (int32_t)(f0 + o);
+        ++k;
+      }
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt_s[0] = carry;
+  }
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < e; base += kT16) {
+      const int t = base + threadIdx.x;
+      const int bl = nb - 1 - t;  // descending blocks
+      uint32_t surv = 0;
+      int64_t f0 = 0;
+      if (t < e) {
+        uint32_t mb, lb;
+        block_flags(bl, mb, lb);
+        surv = ~mb & lb & 0xffffu;
+        const int occ_n = C - bl * 16;
+        const uint32_t occ_bits = occ_n >= 16 ? 0xffffu : occ_n <= 0 ? 0u : ((1u << occ_n) - 1u);
+        evk += __popc(mb & occ_bits);
+        f0 = (int64_t)tab[bl] * 16;
+      }
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(__popc(surv), excl, tot);
+      int64_t k = carry + excl;
+      for (int o = 15; o >= 0; --o) {  // descending positions within the block
+        if (surv >> o & 1u) {
+          mv[2 * k] = (int32_t)(f0 + o);
+          ++k;
+        }
+      }
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt_s[1] = carry;
+  }
+  atomicAdd(&cnt_s[2], evk);
+  __syncthreads();
+  const int32_t nmoves = cnt_s[1];
+  if (nmoves > cnt_s[0]) {
+    if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
+    return;
+  }
+  for (int k = threadIdx.x; k < nmoves; k += kT16) {
+    const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
+    p.metric[dst] = p.metric[src];
+    p.logical[dst] = p.logical[src];
+    p.protected_[dst] = p.protected_[src];
+    p.fresh[dst] = p.fresh[src];
+  }
+  __syncthreads();
+  // ---- free the trailing e blocks and reset their slots ----
+  for (int t = threadIdx.x; t < e; t += kT16) {
+    const int j = rb + t;
+    const int32_t blk = tab[j];
+    const int64_t f0 = (int64_t)blk * 16;
+    float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
+    int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      lp[q] = make_int4(-1, -1, -1, -1);
+    }
+    *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
+    p.free_flag[blk] = 1;
+    atomicAdd(&p.free_tile[blk / KVC_FREE_TILE], 1);
+    if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
+  }
+  const int keep = rb;
+  const int Cn = C < keep * 16 ? C : keep * 16;
+  // ---- logical renumbering: rank among the kept logicals ----
+  const int words = (int)((n + 31) / 32);
+  uint32_t *wpre = bitmap + words;
+  for (int w = threadIdx.x; w < words; w += kT16) bitmap[w] = 0;
+  __syncthreads();
+  const int kb = (Cn + 15) / 16;
+  for (int bl = threadIdx.x; bl < kb; bl += kT16) {
+    const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 l4 = lp[q];
+      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pos = bl * 16 + q * 4 + i;
+        if (pos >= Cn) continue;
+        const int32_t lg = lv[i];
+        if (lg < 0 || lg >= n) {
+          set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+          continue;
+        }
+        const uint32_t bit = 1u << (lg & 31);
+        if (atomicOr(&bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+      }
+    }
+  }
+  __syncthreads();
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < words; base += kT16) {
+      const int w = base + threadIdx.x;
+      const int32_t c = w < words ? __popc(bitmap[w]) : 0;
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(c, excl, tot);
+      if (w < words) wpre[w] = carry + excl;
+      carry += tot;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int bl = threadIdx.x; bl < kb; bl += kT16) {
+    int4 *lp = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int4 l4 = lp[q];
+      int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pos = bl * 16 + q * 4 + i;
+        const int32_t lg = lv[i];
+        if (pos >= Cn || lg < 0 || lg >= n) continue;
+        lv[i] = (int32_t)wpre[lg >> 5] + __popc(bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
+      }
+      lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    p.nblocks[hidx] = keep;
+    p.ctx[hidx] = Cn;
+    if (M.move_counts) M.move_counts[g] = nmoves;
+    if (M.evicted_kvs) M.evicted_kvs[g] = cnt_s[2];
+    if (M.totals) {
+      atomicAdd((unsigned long long *)&M.totals[0], (unsigned long long)e);
+      atomicAdd((unsigned long long *)&M.totals[1], (unsigned long long)cnt_s[2]);
+      atomicAdd((unsigned long long *)&M.totals[2], (unsigned long long)nmoves);
+    }
+  }
+}
+
 // K/V rows of every move of the round: grid (head, part); a warp moves one
 // (K, V) row pair per step with 16-byte lanes, 4 pairs in flight per warp.
 // Sources are inside blocks freed by k_compact; nothing can reuse them before
@@ -693,10 +1022,12 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.cap = sc.take<int32_t>(T);
   S.lo = sc.take<int32_t>(T);
   S.hi = sc.take<int32_t>(T);
+  S.ltc = sc.take<int32_t>(T);
+  S.lec = sc.take<int32_t>(T);
   S.R = sc.take<int32_t>((int64_t)a->n_seqs * kBins);
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
-  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.R || !S.prefix || !S.E) return KVC_ERR_INVALID;
+  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.prefix || !S.E) return KVC_ERR_INVALID;
   return KVC_OK;
 }
 
@@ -735,7 +1066,16 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
     configured = true;
   }
   if (dyn > 200 * 1024) return KVC_ERR_UNSUPPORTED;
-  k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
+  if (pool->block_size == 16) {
+    static bool conf16 = false;
+    if (!conf16) {
+      cudaFuncSetAttribute(k_compact16, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      conf16 = true;
+    }
+    k_compact16<<<(int)T, kT16, dyn, s>>>(*pool, a->seq_rows, S, M);
+  } else {
+    k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
+  }
   if (pool->k_cache) k_copy_kv<<<dim3((unsigned)T, 8), 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts);
   if (a->totals) k_free_total<<<1, 1024, 0, s>>>(*pool, a->totals);
   KVC_CHECK_LAUNCH();

@@ -30,7 +30,6 @@ namespace {
 constexpr int kTileKeys = 128;
 template <int D>
 constexpr int stages_for() { return D >= 256 ? 2 : 4; }
-constexpr int kThreads = 192;  // 6 warps
 
 struct WinParams {
   int L, H, r, wq, RW, D, start;
@@ -38,7 +37,6 @@ struct WinParams {
   float scale;                 // log2(e) / sqrt(d)
   int agg;                     // 1 L1, 2 L2
   float2 *partial;             // [H][chunks][N] (m, z)
-  const float2 *stat;          // [H][N] (M, 1/Z)
   float *raw;                  // [H][L]
 };
 
@@ -101,8 +99,29 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 // ---- the tile pipeline ------------------------------------------------------
 
 template <int N, int D, int PASS>
-__global__ void __launch_bounds__(kThreads, 1)
+struct WinCfg {
+  static constexpr int kEW = PASS == 0 ? 8 : 4;  // epilogue warps (2 per lane quadrant in pass 0)
+  static constexpr int kThreads = 64 + 32 * kEW;
+  static constexpr int kNC = N / (kEW / 4);      // columns per epilogue thread
+};
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int N, int D, int PASS>
+__global__ void __launch_bounds__(WinCfg<N, D, PASS>::kThreads, 1)
     k_window(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, const WinParams P) {
+  using Cfg = WinCfg<N, D, PASS>;
+  constexpr int kEW = Cfg::kEW, kNC = Cfg::kNC, kThr = Cfg::kThreads;
   constexpr int kStages = stages_for<D>();
   constexpr int kAtoms = D / 64;                      // 128-byte K-major column blocks
   constexpr int kTileBytes = kTileKeys * D * 2;       // one K tile
@@ -128,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * kEW); }
     mbar_init(qfull, 1);
     fence_barrier_init();
   }
@@ -138,13 +157,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int c = threadIdx.x; c < N; c += kThreads) {
+  for (int c = threadIdx.x; c < N; c += kThr) {
     const bool real = c < P.RW;
     lim_s[c] = real ? P.start + c % P.wq : -1;
     if (PASS == 1) {
-      const float2 st = P.stat[(int64_t)head * N + c];
-      stat_s[c] = real ? st.x : INFINITY;  // padded columns contribute exp2(-inf) * 0
-      stat_s[N + c] = real ? st.y : 0.f;
+      // fold the statistics partials of every chunk of this head (log-sum-exp)
+      float mm = -INFINITY, zz = 0.f;
+      for (int k = 0; k < P.chunks; ++k) {
+        const float2 q = P.partial[((int64_t)head * P.chunks + k) * N + c];
+        if (q.x == -INFINITY) continue;
+        const float mn = fmaxf(mm, q.x);
+        zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + q.y * exp2f(q.x - mn);
+        mm = mn;
+      }
+      stat_s[c] = real ? mm : INFINITY;  // padded columns contribute exp2(-inf) * 0
+      stat_s[N + c] = (real && zz > 0.f) ? 1.f / zz : 0.f;
     }
   }
   tc_fence_before();
@@ -193,81 +220,74 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5 = TMEM lane quadrants 2,3,0,1) ------
+    // ---------------- epilogue: warp w covers TMEM lane quadrant w%4 and
+    // columns [half*kNC, half*kNC + kNC) ------------------------------------
     const int quad = warp & 3;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int half = (warp - 2) / 4;
+    const int c0 = half * kNC;
+    const int et = threadIdx.x - 64;
     const int key_local = quad * 32 + lane;
-    // pass 0: per-thread online (max, sum exp2) of every column over this
-    // thread's keys; pass 1: M and 1/Z per column from the combine kernel.
-    float m[N], z[N];
+    float m[kNC], z[kNC];
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
-      m[c] = PASS == 0 ? -INFINITY : stat_s[c];
-      z[c] = PASS == 0 ? 0.f : stat_s[N + c];
+    for (int c = 0; c < kNC; ++c) {
+      m[c] = PASS == 0 ? -INFINITY : stat_s[c0 + c];
+      z[c] = PASS == 0 ? 0.f : stat_s[N + c0 + c];
     }
     for (int i = 0; i < ntiles; ++i) {
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i / 2) & 1);
       tc_fence_after();
-      float v[N];
+      float v[kNC];
+      const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * N + c0;
+      if constexpr (kNC == 16) {
+        tmem_ld16(tbase, v);
+      } else {
 #pragma unroll
-      for (int g = 0; g < N / 32; ++g) tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * N + g * 32, v + g * 32);
+        for (int g = 0; g < kNC / 32; ++g) tmem_ld32(tbase + g * 32, v + g * 32);
+      }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);  // 128 arrivals release the accumulator
+      mbar_arrive(&tempty[acc]);  // all epilogue threads arrive: accumulator free
       const int tile0 = (t_lo + i) * kTileKeys;
       const int j = tile0 + key_local;  // key position within the head
       // every window row sees every key of this tile and the tile is inside L
       const bool fast = tile0 + kTileKeys - 1 <= P.start && tile0 + kTileKeys <= P.L;
       if (PASS == 0) {
-        if (fast) {
+        // online (max, sum exp2): the max only moves a few times per column,
+        // so the rescaling branch is rare and most elements cost one exp2
 #pragma unroll
-          for (int c = 0; c < N; ++c) {
+        for (int c = 0; c < kNC; ++c) {
+          if (fast || (j < P.L && j <= lim_s[c0 + c])) {
             const float s = v[c] * P.scale;
-            const float mn = fmaxf(m[c], s);
-            z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
-            m[c] = mn;
-          }
-        } else if (j < P.L) {
-#pragma unroll
-          for (int c = 0; c < N; ++c) {
-            if (j <= lim_s[c]) {
-              const float s = v[c] * P.scale;
-              const float mn = fmaxf(m[c], s);
-              z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
-              m[c] = mn;
+            if (s > m[c]) {
+              z[c] = z[c] * exp2f(m[c] - s) + 1.f;
+              m[c] = s;
+            } else {
+              z[c] += exp2f(s - m[c]);
             }
           }
         }
       } else {
         float contrib = 0.f;
-        if (fast) {
 #pragma unroll
-          for (int c = 0; c < N; ++c) {
-            const float pr = exp2f(v[c] * P.scale - m[c]) * z[c];  // columns >= RW: M=+inf, 1/Z=0
-            contrib += P.agg == 2 ? pr * pr : pr;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < N; ++c) {
-            const float pr = exp2f(v[c] * P.scale - m[c]) * z[c];
-            const float f = P.agg == 2 ? pr * pr : pr;
-            contrib += j <= lim_s[c] ? f : 0.f;
-          }
+        for (int c = 0; c < kNC; ++c) {
+          const float pr = exp2f(v[c] * P.scale - m[c]) * z[c];  // columns >= RW: M=+inf, 1/Z=0
+          const float f = P.agg == 2 ? pr * pr : pr;
+          contrib += (fast || j <= lim_s[c0 + c]) ? f : 0.f;
         }
         if (j < P.L) P.raw[(int64_t)head * P.L + j] = contrib;
       }
     }
     if (PASS == 0) {
-      // combine the 128 threads' (m, z) per column through the (now idle) ring
-      named_sync(1, 128);
+      // combine the (m, z) of all key lanes per column through the idle ring
+      named_sync(1, 32 * kEW);
       float *rm = reinterpret_cast<float *>(ktiles);
       float *rz = rm + 128 * (N + 1);
 #pragma unroll
-      for (int c = 0; c < N; ++c) {
-        rm[et * (N + 1) + c] = m[c];
-        rz[et * (N + 1) + c] = z[c];
+      for (int c = 0; c < kNC; ++c) {
+        rm[key_local * (N + 1) + c0 + c] = m[c];
+        rz[key_local * (N + 1) + c0 + c] = z[c];
       }
-      named_sync(1, 128);
+      named_sync(1, 32 * kEW);
       if (et < N) {
         float mm = -INFINITY, zz = 0.f;
         for (int k = 0; k < 128; ++k) {
@@ -284,20 +304,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-}
-
-__global__ void k_win_combine(WinParams P, int N, float2 *stat) {
-  const int head = blockIdx.x, c = threadIdx.x;
-  if (c >= N) return;
-  float m = -INFINITY, z = 0.f;
-  for (int k = 0; k < P.chunks; ++k) {
-    const float2 q = P.partial[((int64_t)head * P.chunks + k) * N + c];
-    if (q.x == -INFINITY) continue;
-    const float mn = fmaxf(m, q.x);
-    z = (m == -INFINITY ? 0.f : z * exp2f(m - mn)) + q.y * exp2f(q.x - mn);
-    m = mn;
-  }
-  stat[(int64_t)head * N + c] = make_float2(m, z > 0.f ? 1.f / z : 0.f);
 }
 
 // Centred max-pool (truncated at the edges) + per-slot install.
@@ -369,10 +375,8 @@ int run_window(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cud
   }
   if (smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
   dim3 grid(P.chunks, P.H);
-  k0<<<grid, kThreads, smem, s>>>(tmK, tmQ, P);
-  float2 *stat = const_cast<float2 *>(P.stat);
-  k_win_combine<<<P.H, 64, 0, s>>>(P, N, stat);
-  k1<<<grid, kThreads, smem, s>>>(tmK, tmQ, P);
+  k0<<<grid, WinCfg<N, D, 0>::kThreads, smem, s>>>(tmK, tmQ, P);
+  k1<<<grid, WinCfg<N, D, 1>::kThreads, smem, s>>>(tmK, tmQ, P);
   const int gx = (P.L + 255) / 256 < 1184 ? (P.L + 255) / 256 : 1184;
   k_win_pool<<<dim3(gx, P.H), 256, 0, s>>>(*pool, P, a->seq_row, a->layer, a->pool, a->protect_window,
                                            a->metrics_out);
@@ -407,9 +411,8 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   if (!N) return KVC_ERR_UNSUPPORTED;
   Scratch sc(pool);
   P.partial = sc.take<float2>((int64_t)H * chunks * N);
-  P.stat = sc.take<float2>((int64_t)H * N);
   P.raw = sc.take<float>((int64_t)H * a->L);
-  if (!P.partial || !P.stat || !P.raw) return KVC_ERR_INVALID;
+  if (!P.partial || !P.raw) return KVC_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = a->n_layers > 1 ? a->n_layers : 1;
   if (a->layer < 0 || (a->seq_row >= 0 && a->layer + nl > pool->num_layers)) return KVC_ERR_INVALID;
