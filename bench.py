@@ -305,7 +305,8 @@ def decode_bench(S, args, e2e=False):
         res["k1_bytes_mean"] = float(bytes_steps.mean())
         res["k1_gbs"] = float(bytes_steps.sum() / (durs.sum() * 1e-3) / 1e9)
         res["bytes_per_step"] = float(bytes_steps.sum(axis=1).mean())
-        res["launches_per_step"] = 4 + l + 1
+        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream + finish) + fresh clear
+        res["launches_per_step"] = 4 + 2 * l + 1
     else:
         res["h2d"] = int(sum(x.numel() * 2 for x in (hq[0], hk[0], hv[0])))
         res["d2h"] = int(hout.numel() * 2)
@@ -415,6 +416,8 @@ def run_reference(args, rank, world):
     import multiprocessing as mp
 
     cores = os.cpu_count() or 1
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"  # one BLAS thread per worker process: no oversubscription
     L, H, r, d, l = args.context, args.kv_heads, args.group, args.head_dim, args.layers
     ctx_heads = [int(L / args.rate)] * H  # uniform control lengths
     per = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
@@ -509,10 +512,14 @@ def main():
         line["e2e"] = {"value": B * world * steps / (ms_e2e * 1e-3), "unit": UNIT,
                        "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
     if not args.no_cpu:
+        from threadpoolctl import threadpool_limits
+
         ctx = dec["ctx_before"].reshape(B, args.layers, args.kv_heads)
-        t_sl = cpu_decode_sample(ctx[0, 0].tolist(), args.head_dim, args.group, args.kv_heads, args.cpu_seconds / 2)
-        t_ev = cpu_evict_sample(None, args.context, args.kv_heads, 2, args.rate)
-        t_w = cpu_window_sample(args.context, args.kv_heads, args.group, args.head_dim)
+        with threadpool_limits(limits=1):  # the reference is single-threaded Python/numpy
+            t_sl = cpu_decode_sample(ctx[0, 0].tolist(), args.head_dim, args.group, args.kv_heads,
+                                     args.cpu_seconds / 2)
+            t_ev = cpu_evict_sample(None, args.context, args.kv_heads, 2, args.rate)
+            t_w = cpu_window_sample(args.context, args.kv_heads, args.group, args.head_dim)
         line["cpu_baseline"] = {
             "value": 1.0 / (args.layers * t_sl), "unit": UNIT, "cores": 1, "kind": "port",
             "sample": (f"oracle decode_step_layer of one (seq, layer): {args.kv_heads} heads, C={ctx[0, 0].tolist()}, "
