@@ -20,6 +20,7 @@
 //           (the layer's K is re-read from L2: 64 MB at Llama-8B shapes)
 //   pool:  centred max-pool, install metric/logical/protected per slot.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -29,13 +30,14 @@ namespace {
 
 constexpr int kTileKeys = 128;
 template <int D>
-constexpr int stages_for() { return D >= 256 ? 2 : 4; }
+constexpr int stages_for() { return D >= 256 ? 3 : D >= 128 ? 6 : 8; }
 
 struct WinParams {
   int L, H, r, wq, RW, D, start;
   int tiles_per_head, chunks;  // CTA = (chunk, head)
   float scale;                 // log2(e) / sqrt(d)
   int agg;                     // 1 L1, 2 L2
+  int dbg;                     // experiments: bit0 skip pass-0 math
   float2 *partial;             // [H][chunks][N] (m, z)
   float *raw;                  // [H][L]
 };
@@ -47,6 +49,14 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(dst)),
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -98,9 +108,9 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 
 // ---- the tile pipeline ------------------------------------------------------
 
-template <int N, int D, int PASS>
+template <int N, int D, int PASS, int EW = 4>
 struct WinCfg {
-  static constexpr int kEW = PASS == 0 ? 8 : 4;  // epilogue warps (2 per lane quadrant in pass 0)
+  static constexpr int kEW = PASS == 0 ? EW : 4;  // epilogue warps (EW/4 per lane quadrant in pass 0)
   static constexpr int kThreads = 64 + 32 * kEW;
   static constexpr int kNC = N / (kEW / 4);      // columns per epilogue thread
 };
@@ -117,10 +127,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int N, int D, int PASS>
-__global__ void __launch_bounds__(WinCfg<N, D, PASS>::kThreads, 1)
+template <int N, int D, int PASS, int EW, bool LAZY>
+__global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
     k_window(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, const WinParams P) {
-  using Cfg = WinCfg<N, D, PASS>;
+  using Cfg = WinCfg<N, D, PASS, EW>;
   constexpr int kEW = Cfg::kEW, kNC = Cfg::kNC, kThr = Cfg::kThreads;
   constexpr int kStages = stages_for<D>();
   constexpr int kAtoms = D / 64;                      // 128-byte K-major column blocks
@@ -190,8 +200,8 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS>::kThreads, 1)
         if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
         mbar_expect_tx(&full[s], kTileBytes);
         const int row = head * P.L + (t_lo + i) * kTileKeys;
-        for (int a = 0; a < kAtoms; ++a)
-          tma_load_2d(ktiles + s * kTileBytes + a * kTileKeys * 128, &tmK, a * 64, row, &full[s]);
+        // one 3-D box = the whole tile (kTileKeys contiguous rows, all atoms)
+        tma_load_3d(ktiles + s * kTileBytes, &tmK, 0, row, 0, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -251,18 +261,26 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS>::kThreads, 1)
       const int j = tile0 + key_local;  // key position within the head
       // every window row sees every key of this tile and the tile is inside L
       const bool fast = tile0 + kTileKeys - 1 <= P.start && tile0 + kTileKeys <= P.L;
-      if (PASS == 0) {
+      if (PASS == 0 && (P.dbg & 1)) {
+        m[0] = fmaxf(m[0], v[0]);
+      } else if (PASS == 0) {
         // online (max, sum exp2): the max only moves a few times per column,
         // so the rescaling branch is rare and most elements cost one exp2
 #pragma unroll
         for (int c = 0; c < kNC; ++c) {
           if (fast || (j < P.L && j <= lim_s[c0 + c])) {
             const float s = v[c] * P.scale;
-            if (s > m[c]) {
-              z[c] = z[c] * exp2f(m[c] - s) + 1.f;
-              m[c] = s;
+            if (LAZY) {
+              if (s > m[c]) {
+                z[c] = z[c] * exp2f(m[c] - s) + 1.f;
+                m[c] = s;
+              } else {
+                z[c] += exp2f(s - m[c]);
+              }
             } else {
-              z[c] += exp2f(s - m[c]);
+              const float mn = fmaxf(m[c], s);
+              z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
+              m[c] = mn;
             }
           }
         }
@@ -347,6 +365,20 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D bf16 map over [rows][D] with a {64, box_rows} SWIZZLE_128B box.
+// 3-D view {64 elems, rows, D/64 atoms} with a {64, box_rows, D/64} box: one
+// op per tile, contiguous source rows, smem laid out [atom][row][128 B].
+bool make_map3(CUtensorMap *map, const void *base, int64_t rows, int D, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(D / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)(D / 64)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
@@ -362,20 +394,31 @@ bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_r
 template <int N, int D>
 int run_window(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cudaStream_t s) {
   CUtensorMap tmK, tmQ;
-  if (!make_map(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
+  if (!make_map3(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
   if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
   const int smem = stages_for<D>() * kTileKeys * D * 2 + N * D * 2 + N * 4 + 256 + 2 * N * 4 + 1024;
-  auto k0 = k_window<N, D, 0>;
-  auto k1 = k_window<N, D, 1>;
+  // variant (experiments): KVC_K2_EW = 4|8 epilogue warps in pass 0, KVC_K2_LAZY = 0|1
+  static int ew = -1, lazy = -1;
+  if (ew < 0) {
+    const char *e1 = getenv("KVC_K2_EW");
+    const char *e2 = getenv("KVC_K2_LAZY");
+    ew = (e1 && atoi(e1) == 8) ? 8 : 4;
+    lazy = (e2 && atoi(e2) == 1) ? 1 : 0;
+  }
+  auto k1 = k_window<N, D, 1, 4, false>;
+  auto k0 = ew == 8 ? (lazy ? k_window<N, D, 0, 8, true> : k_window<N, D, 0, 8, false>)
+                    : (lazy ? k_window<N, D, 0, 4, true> : k_window<N, D, 0, 4, false>);
+  const int t0 = ew == 8 ? WinCfg<N, D, 0, 8>::kThreads : WinCfg<N, D, 0, 4>::kThreads;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (auto f : {k_window<N, D, 0, 8, true>, k_window<N, D, 0, 8, false>, k_window<N, D, 0, 4, true>,
+                   k_window<N, D, 0, 4, false>, k1})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
   if (smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
   dim3 grid(P.chunks, P.H);
-  k0<<<grid, WinCfg<N, D, 0>::kThreads, smem, s>>>(tmK, tmQ, P);
+  k0<<<grid, t0, smem, s>>>(tmK, tmQ, P);
   k1<<<grid, WinCfg<N, D, 1>::kThreads, smem, s>>>(tmK, tmQ, P);
   const int gx = (P.L + 255) / 256 < 1184 ? (P.L + 255) / 256 : 1184;
   k_win_pool<<<dim3(gx, P.H), 256, 0, s>>>(*pool, P, a->seq_row, a->layer, a->pool, a->protect_window,
@@ -407,6 +450,10 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   P.chunks = chunks;
   P.scale = 1.4426950408889634f / sqrtf((float)D);
   P.agg = a->aggregation == 2 ? 2 : 1;
+  {
+    const char *e = getenv("KVC_K2_DBG");
+    P.dbg = e ? atoi(e) : 0;
+  }
   const int N = P.RW <= 32 ? 32 : P.RW <= 64 ? 64 : 0;
   if (!N) return KVC_ERR_UNSUPPORTED;
   Scratch sc(pool);
