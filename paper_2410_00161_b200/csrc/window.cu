@@ -21,6 +21,7 @@
 //   pool:  centred max-pool, install metric/logical/protected per slot.
 #include <cuda.h>
 #include <stdlib.h>
+#include <stdio.h>
 
 #include "common.cuh"
 
@@ -30,7 +31,7 @@ namespace {
 
 constexpr int kTileKeys = 128;
 template <int D>
-constexpr int stages_for() { return D >= 256 ? 3 : D >= 128 ? 6 : 8; }
+constexpr int stages_for() { return D >= 256 ? 2 : D >= 128 ? 3 : 6; }  // 2 CTAs/SM up to d=128
 
 struct WinParams {
   int L, H, r, wq, RW, D, start;
@@ -40,6 +41,7 @@ struct WinParams {
   int dbg;                     // experiments: bit0 skip pass-0 math
   float2 *partial;             // [H][chunks][N] (m, z)
   float *raw;                  // [H][L]
+  int *bar_cnt;                // [2H] fused-path barrier counters
 };
 
 // ---- PTX wrappers ---------------------------------------------------------
@@ -136,8 +138,9 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
   constexpr int kAtoms = D / 64;                      // 128-byte K-major column blocks
   constexpr int kTileBytes = kTileKeys * D * 2;       // one K tile
   constexpr int kQBytes = N * D * 2;
-  constexpr uint32_t kCols = 2 * N;                   // two TMEM accumulators
-  constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : 128;
+  constexpr int kAcc = 4;                             // TMEM accumulators (MMA runs ahead)
+  constexpr uint32_t kCols = kAcc * N;
+  constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : 256;
   constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -145,7 +148,8 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
   uint8_t *qbuf = smem + kStages * kTileBytes;             // kQBytes
   int *lim_s = reinterpret_cast<int *>(qbuf + kQBytes);  // [N] last visible key per column (-1: pad)
   uint64_t *bars = reinterpret_cast<uint64_t *>(lim_s + N);
-  uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + 2, *qfull = tempty + 2;
+  uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = tfull + kAcc,
+           *qfull = tempty + kAcc;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qfull + 1);
   float *stat_s = reinterpret_cast<float *>(tmem_slot + 4);  // pass 1: M[N], invZ[N]
 
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * kEW); }
+    for (int a = 0; a < kAcc; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * kEW); }
     mbar_init(qfull, 1);
     fence_barrier_init();
   }
@@ -209,15 +213,15 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
     if (ntiles > 0) {
       mbar_wait(qfull, 0);
       for (int i = 0; i < ntiles; ++i) {
-        const int s = i % kStages, acc = i & 1;
+        const int s = i % kStages, acc = i % kAcc;
         mbar_wait(&full[s], (i / kStages) & 1);
-        if (i >= 2) mbar_wait(&tempty[acc], ((i / 2) - 1) & 1);
+        if (i >= kAcc) mbar_wait(&tempty[acc], ((i / kAcc) - 1) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t abase = smem_u32(ktiles + s * kTileBytes);
           const uint32_t bbase = smem_u32(qbuf);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
+          for (int kk = 0; kk < ((P.dbg & 2) ? 0 : D / 16); ++kk) {
             const int atom = kk / 4, sub = kk % 4;
             const uint64_t ad = sw128_desc(abase + atom * kTileKeys * 128 + sub * 32);
             const uint64_t bd = sw128_desc(bbase + atom * N * 128 + sub * 32);
@@ -244,8 +248,8 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
       z[c] = PASS == 0 ? 0.f : stat_s[N + c0 + c];
     }
     for (int i = 0; i < ntiles; ++i) {
-      const int acc = i & 1;
-      mbar_wait(&tfull[acc], (i / 2) & 1);
+      const int acc = i % kAcc;
+      mbar_wait(&tfull[acc], (i / kAcc) & 1);
       tc_fence_after();
       float v[kNC];
       const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * N + c0;
@@ -306,22 +310,313 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
         rz[key_local * (N + 1) + c0 + c] = z[c];
       }
       named_sync(1, 32 * kEW);
-      if (et < N) {
-        float mm = -INFINITY, zz = 0.f;
-        for (int k = 0; k < 128; ++k) {
-          const float qm = rm[k * (N + 1) + et], qz = rz[k * (N + 1) + et];
+      // every epilogue thread folds a slice of one column's 128 entries,
+      // then one thread per column folds the slices
+      constexpr int kSl = 32 * kEW / N;  // slices per column
+      constexpr int kPer = 128 / kSl;
+      float mm = -INFINITY, zz = 0.f;
+      {
+        const int col = et % N, sl = et / N;
+        for (int k = sl * kPer; k < (sl + 1) * kPer; ++k) {
+          const float qm = rm[k * (N + 1) + col], qz = rz[k * (N + 1) + col];
           if (qm == -INFINITY) continue;
           const float mn = fmaxf(mm, qm);
           zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + qz * exp2f(qm - mn);
           mm = mn;
         }
-        P.partial[((int64_t)head * P.chunks + chunk) * N + et] = make_float2(mm, zz);
+      }
+      named_sync(1, 32 * kEW);
+      float2 *sl2 = reinterpret_cast<float2 *>(rm);
+      sl2[et] = make_float2(mm, zz);
+      named_sync(1, 32 * kEW);
+      if (et < N) {
+        float m2 = -INFINITY, z2 = 0.f;
+        for (int k = 0; k < kSl; ++k) {
+          const float2 q = sl2[k * N + et];
+          if (q.x == -INFINITY) continue;
+          const float mn = fmaxf(m2, q.x);
+          z2 = (m2 == -INFINITY ? 0.f : z2 * exp2f(m2 - mn)) + q.y * exp2f(q.x - mn);
+          m2 = mn;
+        }
+        P.partial[((int64_t)head * P.chunks + chunk) * N + et] = make_float2(m2, z2);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// ---------------------------------------------------------------------------
+// Fused single-pass K2 (cooperative launch): every CTA owns <= kMaxT tiles of
+// one head and keeps their score tiles resident in TMEM, so K is read from
+// HBM exactly once.  Per-head grid barriers separate (1) the softmax
+// statistics, (2) the metric of the resident tiles and (3) pooling, which
+// needs its neighbours' raw metrics.
+// ---------------------------------------------------------------------------
+
+struct FusedParams {
+  WinParams w;
+  int cph;            // CTAs per head
+  int tiles_per_cta;  // <= kMaxT
+  int *bar_cnt;       // [2][H] arrival counters (zeroed before launch)
+  kvc_pool p;
+  int row, layer, pool, protect;
+  float *out;
+};
+
+__device__ __forceinline__ void head_barrier(int *cnt, int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1);
+    while (atomicAdd(cnt, 0) < target) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int D>
+constexpr int fused_stages() { return D >= 256 ? 2 : D >= 128 ? 5 : 10; }
+
+// tcgen05 kernels run one CTA per SM here (EIATTR_RESERVED_SMEM_USED), so a
+// CTA owns the whole 512-column TMEM: 16 resident 128x32 score tiles.
+constexpr int kFusedEW = 16;  // epilogue warps: 4 per TMEM lane quadrant
+
+template <int N, int D>
+__global__ void __launch_bounds__(64 + 32 * kFusedEW, 1)
+    k_window_fused(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
+                   const __grid_constant__ CUtensorMap tmK16, const FusedParams F) {
+  constexpr int kEW = kFusedEW, kGroups = kEW / 4, kNC = N / kGroups;
+  constexpr int kStages = fused_stages<D>();
+  constexpr int kAtoms = D / 64;
+  constexpr int kTileBytes = kTileKeys * D * 2;
+  constexpr int kQBytes = N * D * 2;
+  constexpr int kMaxT = 512 / N;  // resident score tiles (all 512 TMEM columns)
+  constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+  const WinParams &P = F.w;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *ktiles = smem;
+  uint8_t *qbuf = smem + kStages * kTileBytes;
+  int *lim_s = reinterpret_cast<int *>(qbuf + kQBytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(lim_s + N);
+  uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *qfull = tfull + kMaxT;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qfull + 1);
+  float *stat_s = reinterpret_cast<float *>(tmem_slot + 4);  // M[N], invZ[N]
+  float *halfsum = stat_s + 2 * N;  // [kGroups-1][kMaxT][128] contributions of column groups >= 1
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int head = blockIdx.x / F.cph, cidx = blockIdx.x % F.cph;
+  const int t_lo = cidx * F.tiles_per_cta;
+  const int t_hi = min(P.tiles_per_head, t_lo + F.tiles_per_cta);
+  const int ntiles = max(0, t_hi - t_lo);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < kMaxT; ++a) mbar_init(&tfull[a], 1);
+    mbar_init(qfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { prefetch_tmap(&tmK); prefetch_tmap(&tmQ); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int c = threadIdx.x; c < N; c += blockDim.x) lim_s[c] = c < P.RW ? P.start + c % P.wq : -1;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int quad = warp & 3;
+  const int half = (warp - 2) / 4;
+  const int c0 = half * kNC;
+  const int et = threadIdx.x - 64;
+  const int key_local = quad * 32 + lane;
+
+  // ================= phase 1: stream K once, scores -> TMEM, statistics =====
+  if (warp == 0) {
+    if (lane == 0 && ntiles > 0) {
+      mbar_expect_tx(qfull, kQBytes);
+      for (int a = 0; a < kAtoms; ++a) tma_load_2d(qbuf + a * N * 128, &tmQ, a * 64, head * P.RW, qfull);
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kTileBytes);
+        const int row0 = head * P.L + (t_lo + i) * kTileKeys;
+        if (P.dbg & 4) {
+          // 16-row boxes (many small ops in flight) into the same [atom][row] layout
+          for (int rg = 0; rg < kTileKeys / 16; ++rg)
+            for (int a = 0; a < kAtoms; ++a)
+              tma_load_2d(ktiles + s * kTileBytes + a * kTileKeys * 128 + rg * 16 * 128, &tmK16, a * 64,
+                          row0 + rg * 16, &full[s]);
+        } else {
+          tma_load_3d(ktiles + s * kTileBytes, &tmK, 0, row0, 0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (ntiles > 0) {
+      mbar_wait(qfull, 0);
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % kStages;
+        mbar_wait(&full[s], (i / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t abase = smem_u32(ktiles + s * kTileBytes);
+          const uint32_t bbase = smem_u32(qbuf);
+#pragma unroll
+          for (int kk = 0; kk < ((P.dbg & 2) ? 0 : D / 16); ++kk) {
+            const int atom = kk / 4, sub = kk % 4;
+            mma_bf16(tmem + i * N, sw128_desc(abase + atom * kTileKeys * 128 + sub * 32),
+                     sw128_desc(bbase + atom * N * 128 + sub * 32), kIdesc, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&tfull[i]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    float m[kNC], z[kNC];
+#pragma unroll
+    for (int c = 0; c < kNC; ++c) { m[c] = -INFINITY; z[c] = 0.f; }
+    for (int i = 0; i < ntiles; ++i) {
+      mbar_wait(&tfull[i], 0);
+      tc_fence_after();
+      float v[kNC];
+      const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + i * N + c0;
+      if constexpr (kNC == 16) tmem_ld16(tb, v);
+      else tmem_ld32(tb, v);
+      const int tile0 = (t_lo + i) * kTileKeys;
+      const int j = tile0 + key_local;
+      const bool fast = tile0 + kTileKeys - 1 <= P.start && tile0 + kTileKeys <= P.L;
+      if (P.dbg & 1) { m[0] = fmaxf(m[0], v[0]); continue; }
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        if (fast || (j < P.L && j <= lim_s[c0 + c])) {
+          const float s = v[c] * P.scale;
+          const float mn = fmaxf(m[c], s);
+          z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
+          m[c] = mn;
+        }
+      }
+    }
+    // CTA combine through the idle ring, then one partial per column
+    named_sync(1, 32 * kEW);
+    float *rm = reinterpret_cast<float *>(ktiles);
+    float *rz = rm + 128 * (N + 1);
+#pragma unroll
+    for (int c = 0; c < kNC; ++c) {
+      rm[key_local * (N + 1) + c0 + c] = m[c];
+      rz[key_local * (N + 1) + c0 + c] = z[c];
+    }
+    named_sync(1, 32 * kEW);
+    constexpr int kSl = 32 * kEW / N, kPer = 128 / kSl;
+    float mm = -INFINITY, zz = 0.f;
+    {
+      const int col = et % N, sl = et / N;
+      for (int k = sl * kPer; k < (sl + 1) * kPer; ++k) {
+        const float qm = rm[k * (N + 1) + col], qz = rz[k * (N + 1) + col];
+        if (qm == -INFINITY) continue;
+        const float mn = fmaxf(mm, qm);
+        zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + qz * exp2f(qm - mn);
+        mm = mn;
+      }
+    }
+    named_sync(1, 32 * kEW);
+    float2 *sl2 = reinterpret_cast<float2 *>(rm);
+    sl2[et] = make_float2(mm, zz);
+    named_sync(1, 32 * kEW);
+    if (et < N) {
+      float m2 = -INFINITY, z2 = 0.f;
+      for (int k = 0; k < kSl; ++k) {
+        const float2 q = sl2[k * N + et];
+        if (q.x == -INFINITY) continue;
+        const float mn = fmaxf(m2, q.x);
+        z2 = (m2 == -INFINITY ? 0.f : z2 * exp2f(m2 - mn)) + q.y * exp2f(q.x - mn);
+        m2 = mn;
+      }
+      P.partial[((int64_t)head * F.cph + cidx) * N + et] = make_float2(m2, z2);
+    }
+  }
+  head_barrier(&F.bar_cnt[head], F.cph);
+
+  // ================= phase 2: head statistics, metric of resident tiles =======
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    float mm = -INFINITY, zz = 0.f;
+    for (int k = 0; k < F.cph; ++k) {
+      const float2 q = __ldcg(P.partial + ((int64_t)head * F.cph + k) * N + c);  // written by other CTAs
+      if (q.x == -INFINITY) continue;
+      const float mn = fmaxf(mm, q.x);
+      zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + q.y * exp2f(q.x - mn);
+      mm = mn;
+    }
+    const bool real = c < P.RW;
+    stat_s[c] = real ? mm : INFINITY;
+    stat_s[N + c] = (real && zz > 0.f) ? 1.f / zz : 0.f;
+  }
+  __syncthreads();
+  if (warp >= 2) {
+    tc_fence_after();
+    for (int i = 0; i < ntiles; ++i) {
+      float v[kNC];
+      const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + i * N + c0;
+      if constexpr (kNC == 16) tmem_ld16(tb, v);
+      else tmem_ld32(tb, v);
+      const int tile0 = (t_lo + i) * kTileKeys;
+      const int j = tile0 + key_local;
+      const bool fast = tile0 + kTileKeys - 1 <= P.start;
+      float contrib = 0.f;
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        const float pr = exp2f(v[c] * P.scale - stat_s[c0 + c]) * stat_s[N + c0 + c];
+        const float f = P.agg == 2 ? pr * pr : pr;
+        contrib += (fast || j <= lim_s[c0 + c]) ? f : 0.f;
+      }
+      if (half > 0) halfsum[((half - 1) * kMaxT + i) * 128 + key_local] = contrib;
+      named_sync(2, 32 * kEW);
+      if (half == 0 && j < P.L) {
+        for (int gq = 1; gq < kGroups; ++gq) contrib += halfsum[((gq - 1) * kMaxT + i) * 128 + key_local];
+        P.raw[(int64_t)head * P.L + j] = contrib;
+      }
+    }
+  }
+  head_barrier(&F.bar_cnt[P.H + head], F.cph);
+
+  // ================= phase 3: centred max-pool + per-slot install ===========
+  {
+    const int half_p = F.pool / 2;
+    const float *raw = P.raw + (int64_t)head * P.L;
+    const int64_t hidx = F.row >= 0 ? head_index(F.p, F.row, F.layer, head) : 0;
+    const int C = F.row >= 0 ? F.p.ctx[hidx] : 0;
+    const int b = F.p.block_size;
+    const int j_lo = t_lo * kTileKeys, j_hi = min(P.L, t_hi * kTileKeys);
+    // stage this CTA's raw range plus the pooling halo in (idle) shared memory
+    float *rs = reinterpret_cast<float *>(ktiles);
+    const int s_lo = max(0, j_lo - half_p), s_hi = min(P.L, j_hi + half_p);
+    for (int t = s_lo + threadIdx.x; t < s_hi; t += blockDim.x) rs[t - s_lo] = __ldcg(raw + t);
+    __syncthreads();
+    for (int j = j_lo + threadIdx.x; j < j_hi; j += blockDim.x) {
+      float mx = rs[j - s_lo];
+      const int lo = j - half_p < 0 ? 0 : j - half_p;
+      const int hi = j + half_p >= P.L ? P.L - 1 : j + half_p;
+      for (int t = lo; t <= hi; ++t) mx = fmaxf(mx, rs[t - s_lo]);
+      if (F.out) F.out[(int64_t)head * P.L + j] = mx;
+      if (F.row >= 0 && j < C) {
+        const int64_t f = (int64_t)head_table(F.p, hidx)[j / b] * b + j % b;
+        F.p.metric[f] = mx;
+        F.p.logical[f] = j;
+        F.p.protected_[f] = (F.protect && j >= P.start) ? 1 : 0;
+        F.p.fresh[f] = 0;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // Centred max-pool (truncated at the edges) + per-slot install.
@@ -392,7 +687,88 @@ bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_r
 }
 
 template <int N, int D>
+int run_fused(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cudaStream_t s, int *bar_cnt) {
+  constexpr int kMaxT = 512 / N;
+  auto fn = k_window_fused<N, D>;
+  const int smem = fused_stages<D>() * kTileKeys * D * 2 + N * D * 2 + N * 4 + 256 + 2 * N * 4 + (kFusedEW / 4) * kMaxT * 128 * 4 + 1024;
+  static bool configured = false;
+  static int capacity = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int per_sm = 0, dev = 0, nsm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 64 + 32 * kFusedEW, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    per_sm = per_sm > 1 ? 1 : per_sm;  // 512 TMEM columns per CTA
+    capacity = per_sm * nsm;
+    configured = true;
+  }
+  if (getenv("KVC_DEBUG")) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 64 + 32 * kFusedEW, smem);
+    cudaFuncAttributes at;
+    cudaFuncGetAttributes(&at, fn);
+    for (int sm2 : {100000, 90000, 60000, 30000}) {
+      int ps = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, 64 + 32 * 8, sm2);
+      int ps2 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps2, fn, 64, sm2);
+      fprintf(stderr, "[kvc]   smem %d -> per_sm %d (64 thr: %d)\n", sm2, ps, ps2);
+    }
+    fprintf(stderr, "[kvc] fused K2: smem %d capacity %d per_sm %d regs %d static %zu maxdyn %d maxthr %d\n", smem,
+            capacity, per_sm, at.numRegs, at.sharedSizeBytes, at.maxDynamicSharedSizeBytes, at.maxThreadsPerBlock);
+  }
+  if (capacity < 1 || smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
+  const int total = P.H * P.tiles_per_head;
+  int tpc = (total + capacity - 1) / capacity;
+  if (tpc < 1) tpc = 1;
+  while (tpc <= kMaxT && P.H * ((P.tiles_per_head + tpc - 1) / tpc) > capacity) ++tpc;
+  if (tpc > kMaxT) return KVC_ERR_UNSUPPORTED;  // scores do not fit in TMEM: two-pass path
+  const int cph = (P.tiles_per_head + tpc - 1) / tpc;
+  CUtensorMap tmK, tmQ;
+  if (!make_map3(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
+  if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
+  CUtensorMap tmK16;
+  if (!make_map(&tmK16, a->k, (int64_t)P.H * P.L, D, 16)) return KVC_ERR_CUDA;
+  FusedParams F;
+  F.w = P;
+  F.cph = cph;
+  F.tiles_per_cta = tpc;
+  F.bar_cnt = bar_cnt;
+  F.p = *pool;
+  F.row = a->seq_row;
+  F.layer = a->layer;
+  F.pool = a->pool;
+  F.protect = a->protect_window;
+  F.out = a->metrics_out;
+  cudaMemsetAsync(bar_cnt, 0, 2 * P.H * sizeof(int), s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.H * cph);
+  cfg.blockDim = dim3(64 + 32 * kFusedEW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: per-head grid barriers
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, tmK, tmQ, tmK16, F) == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
+}
+
+template <int N, int D>
 int run_window(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cudaStream_t s) {
+  {
+    static int fused_off = -1;
+    if (fused_off < 0) {
+      const char *e = getenv("KVC_K2_TWOPASS");
+      fused_off = (e && atoi(e) == 1) ? 1 : 0;
+    }
+    if (!fused_off && D <= 128 && P.bar_cnt) {
+      const int rc = run_fused<N, D>(pool, a, P, s, P.bar_cnt);
+      if (rc != KVC_ERR_UNSUPPORTED) return rc;
+    }
+  }
   CUtensorMap tmK, tmQ;
   if (!make_map3(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
   if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
@@ -445,7 +821,9 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   P.D = D;
   P.start = a->L - P.wq;
   P.tiles_per_head = (a->L + kTileKeys - 1) / kTileKeys;
-  int chunks = 148 / H > 0 ? 148 / H : 1;  // one wave: 1 CTA per SM
+  // one wave of CTAs (2 per SM when the ring fits twice in shared memory)
+  const int per_sm = D <= 128 ? 2 : 1;
+  int chunks = per_sm * 148 / H > 0 ? per_sm * 148 / H : 1;
   if (chunks > P.tiles_per_head) chunks = P.tiles_per_head;
   P.chunks = chunks;
   P.scale = 1.4426950408889634f / sqrtf((float)D);
@@ -457,8 +835,9 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   const int N = P.RW <= 32 ? 32 : P.RW <= 64 ? 64 : 0;
   if (!N) return KVC_ERR_UNSUPPORTED;
   Scratch sc(pool);
-  P.partial = sc.take<float2>((int64_t)H * chunks * N);
+  P.partial = sc.take<float2>((int64_t)H * (chunks > 304 ? chunks : 304) * N);
   P.raw = sc.take<float>((int64_t)H * a->L);
+  P.bar_cnt = sc.take<int>(2 * H);
   if (!P.partial || !P.raw) return KVC_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = a->n_layers > 1 ? a->n_layers : 1;

@@ -35,4 +35,12 @@ def run_smoke():
         assert err < 1e-2, err  # bf16 P in the P.V MMA
     dst = rig.to_oracle()
     assert np.allclose(dst.metric, st.metric, rtol=1e-3, atol=1e-6)
-    print("smoke: decode parity ok")
+    # one compression round on the device metrics: schedule must be bit-exact
+    st.metric = dst.metric.copy()
+    rig.store.clear_fresh(rig.tables, seqs)
+    O.clear_fresh(st)
+    budgets = {s: O.budget_to_blocks(100, layers, heads, b, st.block_count(s)) for s in seqs}
+    got = K.compress(rig.cache, rig.tables, rig.manager, rig.store, budgets).to_dict()
+    want = O.compress(st, budgets)
+    assert got == want, "compress schedule differs from the oracle"
+    print("smoke: decode + compress parity ok")
