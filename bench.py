@@ -302,7 +302,9 @@ def decode_bench(S, args, e2e=False):
     if S.get("dist"):
         S["dist"].barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = Clocks(torch.cuda.current_device() if not os.environ.get("CUDA_VISIBLE_DEVICES") else 0)
+    cvd = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+    cur = torch.cuda.current_device()
+    clocks = Clocks(int(cvd[cur]) if cur < len(cvd) and cvd[cur].strip().isdigit() else cur)
     with clocks:
         torch.cuda.synchronize()
         t0.record()

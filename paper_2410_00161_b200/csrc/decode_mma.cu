@@ -52,7 +52,10 @@ struct Params {
   int n_ck;         // chunks per (sequence, head) upper bound
   int n_items;
   float scale;      // log2(e)/sqrt(d)
-  int *counter;     // work queue head (zeroed by kernel B for the next call)
+  int *counter;     // work queue head (reset by k_decode_bump for the next call)
+  int *pair_done;   // [pairs] items completed per (sequence, head)
+  int fuse_finish;  // 1: the warp completing a pair's last item finishes it (no kernel B)
+  int counter_ready;
   float *scores;    // [pairs][max_ctx_pad][r]
   float *part_ml;   // [pairs][n_ck][2][kHP]
   float *part_o;    // [pairs][n_ck][r][D]
@@ -156,6 +159,124 @@ __device__ void fetch_item(const Params &P, WItem &w, int lane) {
     w.id = id; w.bi = bi; w.head = head; w.t0 = t0; w.t1 = t1; w.c_old = c_old; w.nblk = nblk; w.hidx = hidx;
   }
   __syncwarp();
+}
+
+// One warp finishes a (sequence, KV head) once all its items are in:
+// merge the split partials (log-sum-exp), write the output and fold
+// f(exp2(s - M) / Z) into every attended slot's metric (reference:
+// attention.py:92-127 output, metrics.py:189-211 accumulation; the appended
+// slot gets metric/logical/fresh, metrics.py:153-158).  ctx is bumped later
+// by k_decode_bump (other warps may still be reading it).
+template <int D>
+__device__ void finish_pair(const Params &P, int bi, int head, int c_old, int lane) {
+  const kvc_pool &p = P.p;
+  const int H = p.num_kv_heads, r = P.r, n_q = H * r;
+  const int pair = bi * H + head;
+  const bool append = P.k_new != nullptr;
+  const int cp = c_old + (append ? 1 : 0);
+  const int nck = (cp + kItemTok - 1) / kItemTok;
+  const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
+  {
+    // NumericError: non-finite query (attention.py:33-36, 108)
+    const uint16_t *qg = P.q + ((int64_t)bi * n_q + head * r) * D;
+    bool bad = false;
+    for (int e = lane; e < r * D; e += 32) bad |= !isfinite(bf16_bits_to_f32(qg[e]));
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)pair, 0);
+  }
+  // lane h < kHP: head statistics
+  float M = -INFINITY, Z = 0.f;
+  if (lane < kHP) {
+    for (int c = 0; c < nck; ++c) M = fmaxf(M, __ldcg(pml + c * 2 * kHP + lane));
+    for (int c = 0; c < nck; ++c) {
+      const float m = __ldcg(pml + c * 2 * kHP + lane);
+      if (m != -INFINITY) Z += __ldcg(pml + c * 2 * kHP + kHP + lane) * exp2f(m - M);
+    }
+  }
+  float Mh[kHP], iZ[kHP];
+#pragma unroll
+  for (int h = 0; h < kHP; ++h) {
+    Mh[h] = __shfl_sync(0xffffffffu, M, h);
+    const float z = __shfl_sync(0xffffffffu, Z, h);
+    iZ[h] = z > 0.f ? 1.f / z : 0.f;
+  }
+  // output (r x D)
+  const float *po = P.part_o + (int64_t)pair * P.n_ck * r * D;
+  for (int e = lane; e < r * D; e += 32) {
+    const int h = e / D;
+    float mh = Mh[0];
+#pragma unroll
+    for (int k = 1; k < kHP; ++k) mh = h == k ? Mh[k] : mh;
+    float izh = iZ[0];
+#pragma unroll
+    for (int k = 1; k < kHP; ++k) izh = h == k ? iZ[k] : izh;
+    float s = 0.f;
+    for (int c = 0; c < nck; ++c) {
+      const float m = __ldcg(pml + c * 2 * kHP + h);
+      if (m != -INFINITY) s += __ldcg(po + (int64_t)c * r * D + e) * exp2f(m - mh);
+    }
+    const float o = s * izh;
+    const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
+    if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
+    else reinterpret_cast<__nv_bfloat16 *>(P.out)[oi] = __float2bfloat16(o);
+  }
+  // metric / rows over every attended position
+  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
+  const int32_t *tab = head_table(p, hidx);
+  const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
+  if (P.metric_mode || P.rows_out) {
+    for (int pos = lane; pos < cp; pos += 32) {
+      float contrib = 0.f;
+      for (int h = 0; h < r; ++h) {
+        float mh = Mh[0], izh = iZ[0];
+#pragma unroll
+        for (int k = 1; k < kHP; ++k) {
+          mh = h == k ? Mh[k] : mh;
+          izh = h == k ? iZ[k] : izh;
+        }
+        const float w = exp2f(__ldcg(srow + (int64_t)pos * r + h) - mh) * izh;
+        contrib += P.metric_mode == 2 ? w * w : w;
+        if (P.rows_out) P.rows_out[(((int64_t)bi * H + head) * r + h) * P.rows_stride + pos] = w;
+      }
+      if (P.metric_mode) {
+        const int64_t slot = (int64_t)tab[pos / kBlk] * kBlk + pos % kBlk;
+        if (append && pos == c_old) {
+          p.metric[slot] = contrib;
+          p.logical[slot] = c_old;
+          p.protected_[slot] = 0;
+          p.fresh[slot] = P.append_fresh ? 1 : 0;
+        } else {
+          p.metric[slot] += contrib;
+        }
+      }
+    }
+  }
+  if (append && !P.metric_mode && p.metric && lane == 0) {
+    const int64_t slot = (int64_t)tab[c_old / kBlk] * kBlk + c_old % kBlk;
+    p.metric[slot] = 0.f;
+    p.logical[slot] = c_old;
+    p.protected_[slot] = 0;
+    p.fresh[slot] = P.append_fresh ? 1 : 0;
+  }
+}
+
+// After kernel A: status checks for heads that produced no item, C += 1 for
+// appends, and the queue / per-pair counters reset for the next launch.
+__global__ void k_decode_bump(const Params P) {
+  const kvc_pool &p = P.p;
+  const int H = p.num_kv_heads;
+  const int pairs = P.batch * H;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *P.counter = 0;
+  if (i >= pairs) return;
+  P.pair_done[i] = 0;
+  const int bi = i / H, head = i % H;
+  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
+  const int c_old = p.ctx[hidx];
+  const bool append = P.k_new != nullptr;
+  const int cp = c_old + (append ? 1 : 0);
+  if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
+  else if (cp > p.nblocks[hidx] * kBlk) set_status(p.status, append ? KVC_DEV_ALLOCATION_ORDER : KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, c_old);
+  else if (append) p.ctx[hidx] = c_old + 1;
 }
 
 template <int D>
@@ -343,6 +464,19 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       }
     }
     (void)item_id;
+    // last item of this (sequence, head)?  then this warp finishes the pair
+    if (P.fuse_finish) {
+      __threadfence();  // this item's scores + partial are visible device-wide
+      __syncwarp();
+      const int n_it = (c_old + (append ? 1 : 0) + kItemTok - 1) / kItemTok;
+      int last = 0;
+      if (lane == 0 && P.fuse_finish) last = atomicAdd(&P.pair_done[pair], 1) == n_it - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        finish_pair<D>(P, bi, head, c_old, lane);
+      }
+    }
     // advance: the fetched-ahead item becomes current; refill the other slot
     const int fin = cur;
     cur ^= 1;
@@ -376,14 +510,7 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
     for (int e = threadIdx.x; e < r * D; e += blockDim.x) bad |= !isfinite(bf16_bits_to_f32(qg[e]));
     if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
   }
-  if (cp < 1 || cp > p.nblocks[hidx] * kBlk) {
-    if (threadIdx.x == 0) {
-      if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
-      else if (append) set_status(p.status, KVC_DEV_ALLOCATION_ORDER, (int32_t)hidx, c_old);
-      else set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, cp);
-    }
-    return;
-  }
+  if (cp < 1 || cp > p.nblocks[hidx] * kBlk) return;  // reported by k_decode_bump
   const int nck = (cp + kItemTok - 1) / kItemTok;
   const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
   if (threadIdx.x < kHP) {
@@ -406,7 +533,15 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   for (int e = threadIdx.x; e < r * D; e += blockDim.x) {
     const int h = e / D;
     float s = 0.f;
-    for (int c = 0; c < nck; ++c) s += po[(int64_t)c * r * D + e] * fac[c * kHP + h];
+    // independent partial loads in flight (the sum order is fixed: deterministic)
+    float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+    int c = 0;
+    for (; c + 4 <= nck; c += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc4[u] += __ldcg(po + (int64_t)(c + u) * r * D + e) * fac[(c + u) * kHP + h];
+    }
+    for (; c < nck; ++c) acc4[0] += __ldcg(po + (int64_t)c * r * D + e) * fac[c * kHP + h];
+    s = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
     const float o = s * iZ[h];
     const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
     if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
@@ -443,8 +578,6 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
     p.protected_[slot] = 0;
     p.fresh[slot] = P.append_fresh ? 1 : 0;
   }
-  __syncthreads();
-  if (append && threadIdx.x == 0) p.ctx[hidx] = c_old + 1;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -519,11 +652,19 @@ int launch(Params &P, cudaStream_t s) {
   if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
   int grid = n_sm * per_sm;
   if (grid > P.n_items) grid = P.n_items;
-  cudaMemsetAsync(P.counter, 0, sizeof(int), s);
+  // Finishing inside kernel A (one warp per pair) measured slower than the
+  // 256-thread finish kernel; KVC_K1_FUSED_FINISH=1 selects it for experiments.
+  static const bool fused_finish = getenv("KVC_K1_FUSED_FINISH") != nullptr;
+  P.fuse_finish = fused_finish ? 1 : 0;
+  if (!P.counter_ready) cudaMemsetAsync(P.counter, 0, (1 + P.batch * P.p.num_kv_heads) * sizeof(int), s);
   fa<<<grid, kThreads, smem, s>>>(tmK, tmV, P);
-  const int smem_b = (2 + P.n_ck) * kHP * 4;
-  if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
-  fb<<<P.batch * P.p.num_kv_heads, 256, smem_b, s>>>(P);
+  if (!P.fuse_finish) {
+    const int smem_b = (2 + P.n_ck) * kHP * 4;
+    if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
+    fb<<<P.batch * P.p.num_kv_heads, 256, smem_b, s>>>(P);
+  }
+  const int pairs = P.batch * P.p.num_kv_heads;
+  k_decode_bump<<<(pairs + 255) / 256, 256, 0, s>>>(P);
   return cudaGetLastError() == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
 }
 
@@ -535,7 +676,8 @@ static int64_t kvc_decode_mma_scratch(const kvc_pool *pool, int batch, int r, in
   const int64_t pairs = (int64_t)batch * pool->num_kv_heads;
   const int64_t ctxp = ((int64_t)max_ctx + kItemTok - 1) / kItemTok * kItemTok;
   const int64_t nck = ctxp / kItemTok;
-  return 256 + pairs * ctxp * r * 4 + pairs * nck * 2 * kHP * 4 + pairs * nck * r * pool->head_dim * 4 + 4096;
+  return (1 + pairs) * 4 + 256 + pairs * ctxp * r * 4 + pairs * nck * 2 * kHP * 4 + pairs * nck * r * pool->head_dim * 4 +
+         4096;
 }
 
 extern "C" int64_t kvc_decode_scratch_bytes(const kvc_pool *pool, int32_t batch, int32_t num_query_heads,
@@ -574,8 +716,10 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.n_items = P.n_ck * a->batch * H;
   P.scale = 1.4426950408889634f / sqrtf((float)D);
   char *base = reinterpret_cast<char *>(pool->scratch);
-  P.counter = reinterpret_cast<int *>(base);  // work-queue head, zeroed per launch
-  int64_t off = 256;
+  P.counter = reinterpret_cast<int *>(base);  // work-queue head + per-pair counters, zeroed per launch
+  P.pair_done = P.counter + 1;
+  P.counter_ready = 0;
+  int64_t off = ((int64_t)(1 + a->batch * H) * 4 + 255) / 256 * 256;
   P.scores = reinterpret_cast<float *>(base + off);
   off += (int64_t)a->batch * H * P.max_ctx_pad * r * 4;
   P.part_ml = reinterpret_cast<float *>(base + off);
