@@ -490,6 +490,55 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
   }
 }
 
+// Metric update for four consecutive positions per thread: R float4 score
+// loads (the 4*R scores are contiguous), one float4 metric read-modify-write
+// (four slots of one block are contiguous in the pool).
+template <int R>
+__device__ __forceinline__ void metric_quads(const Params &P, const float *srow, const int32_t *tab,
+                                             const float *Ms, const float *iZ, int cp, int c_old, bool append) {
+  const kvc_pool &p = P.p;
+  float ms[R], iz[R];
+#pragma unroll
+  for (int h = 0; h < R; ++h) ms[h] = Ms[h], iz[h] = iZ[h];
+  const int nq = (cp + 3) / 4;
+  for (int g = threadIdx.x; g < nq; g += blockDim.x) {
+    const int p0 = g * 4;
+    float sc[4 * R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float4 v = *reinterpret_cast<const float4 *>(srow + (int64_t)p0 * R + 4 * j);
+      sc[4 * j] = v.x, sc[4 * j + 1] = v.y, sc[4 * j + 2] = v.z, sc[4 * j + 3] = v.w;
+    }
+    float c[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      float a = 0.f;
+#pragma unroll
+      for (int h = 0; h < R; ++h) {
+        const float w = exp2f(sc[o * R + h] - ms[h]) * iz[h];
+        a += P.metric_mode == 2 ? w * w : w;
+      }
+      c[o] = a;
+    }
+    const int64_t f0 = (int64_t)tab[p0 / kBlk] * kBlk + p0 % kBlk;
+    float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
+    float4 m4 = *mp;
+    float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int pos = p0 + e;
+      if (pos < cp) mv[e] = (append && pos == c_old) ? c[e] : mv[e] + c[e];
+    }
+    *mp = make_float4(mv[0], mv[1], mv[2], mv[3]);
+    if (append && c_old >= p0 && c_old < p0 + 4) {
+      const int64_t slot = f0 + (c_old - p0);
+      p.logical[slot] = c_old;
+      p.protected_[slot] = 0;
+      p.fresh[slot] = P.append_fresh ? 1 : 0;
+    }
+  }
+}
+
 // Kernel B: per (sequence, head): merge partials, output, metric, C += 1.
 template <int D>
 __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
@@ -550,7 +599,14 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   // metric / rows over all attended positions
   const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
   const int32_t *tab = head_table(p, hidx);
-  if (P.metric_mode || P.rows_out) {
+  if (P.metric_mode && !P.rows_out && (r == 1 || r == 2 || r == 4 || r == 8)) {
+    switch (r) {
+      case 1: metric_quads<1>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
+      case 2: metric_quads<2>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
+      case 4: metric_quads<4>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
+      default: metric_quads<8>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
+    }
+  } else if (P.metric_mode || P.rows_out) {
     for (int pos = threadIdx.x; pos < cp; pos += blockDim.x) {
       float contrib = 0.f;
       for (int h = 0; h < r; ++h) {
