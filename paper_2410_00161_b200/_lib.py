@@ -54,7 +54,7 @@ class DecodeArgs(ctypes.Structure):
         ("seq_rows", _p), ("batch", _i32), ("layer", _i32), ("num_query_heads", _i32),
         ("q", _p), ("k_new", _p), ("v_new", _p), ("out", _p), ("out_f32", _i32),
         ("rows_out", _p), ("rows_stride", _i64), ("metric_mode", _i32), ("append_fresh", _i32),
-        ("max_ctx", _i32), ("splits", _i32),
+        ("max_ctx", _i32), ("splits", _i32), ("queue", _p),
     ]
 
 
@@ -165,6 +165,7 @@ class DeviceContext:
         self.device = device
         self.status = torch.zeros(4, dtype=torch.int32, device=device)
         self._scratch = torch.empty(1 << 22, dtype=torch.uint8, device=device)
+        self._queues: dict = {}
 
     @classmethod
     def get(cls, device) -> "DeviceContext":
@@ -173,6 +174,15 @@ class DeviceContext:
         if key not in cls._by_device:
             cls._by_device[key] = cls(torch.device("cuda", key[1]))
         return cls._by_device[key]
+
+    def decode_queue(self, n: int, stream: int) -> torch.Tensor:
+        """Zeroed int32 work-queue counters for kvc_paged_decode on `stream`
+        (the call leaves them zero, so they are allocated once per stream,
+        not cleared per call)."""
+        qt = self._queues.get(stream)
+        if qt is None or qt.numel() < n:
+            qt = self._queues[stream] = torch.zeros(max(n, 1024), dtype=torch.int32, device=self.device)
+        return qt
 
     def scratch(self, nbytes: int) -> torch.Tensor:
         if self._scratch.numel() < nbytes:

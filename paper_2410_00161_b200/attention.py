@@ -92,8 +92,9 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     p = pool_struct(cache=cache, tables=tables, store=store)
     need = _lib.lib().kvc_decode_scratch_bytes(ctypes.byref(p), B, cfg.num_query_heads, a.max_ctx)
     with_scratch(p, dev, need)
-    _lib.check(_lib.lib().kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)),
-               "paged_decode")
+    stream = _lib.stream_ptr(dev)
+    a.queue = _lib.DeviceContext.get(dev).decode_queue(1 + B * tables.num_kv_heads, stream or 0).data_ptr()
+    _lib.check(_lib.lib().kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), stream), "paged_decode")
     return out
 
 

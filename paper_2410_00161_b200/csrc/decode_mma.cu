@@ -61,6 +61,11 @@ struct Params {
   float *part_o;    // [pairs][n_ck][r][D]
 };
 
+// Programmatic dependent launch: the finish and bump kernels are launched
+// while kernel A drains; they block here until A's writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void tma3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar,
                                       uint64_t pol) {
   asm volatile(
@@ -265,6 +270,8 @@ __global__ void k_decode_bump(const Params P) {
   const kvc_pool &p = P.p;
   const int H = p.num_kv_heads;
   const int pairs = P.batch * H;
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) *P.counter = 0;
   if (i >= pairs) return;
@@ -306,6 +313,8 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
   }
   __syncwarp();
+  pdl_wait();     // the previous kernel's writes (ctx, tables, q, queue) are visible
+  pdl_trigger();  // let kernel B's CTAs launch and park in griddepcontrol.wait
   const uint64_t pol = policy_evict_first();
   fetch_item(P, wit[0], lane);
   fetch_item(P, wit[1], lane);
@@ -548,6 +557,8 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   const int pair = blockIdx.x;
   const int H = p.num_kv_heads, r = P.r, n_q = H * r;
   const int bi = pair / H, head = pair % H;
+  pdl_wait();
+  pdl_trigger();
   const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
   const int c_old = p.ctx[hidx];
   const bool append = P.k_new != nullptr;
@@ -678,6 +689,26 @@ static bool pool_map(CUtensorMap *out, const void *base, int64_t rows, int D) {
   return true;
 }
 
+static bool pdl_off() {
+  static const bool off = getenv("KVC_NO_PDL") != nullptr;
+  return off;
+}
+
+static void launch_pdl(void (*fn)(const Params), int grid, int threads, int smem, cudaStream_t s, const Params &P) {
+  const bool off = pdl_off();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  cudaLaunchKernelEx(&cfg, fn, P);
+}
+
 int stream_smem(int D, int stages) {
   return kNW * stages * 2 * kBlk * D * 2 + kNW * stages * 8 + kNW * 2 * (int)sizeof(WItem) + 1024 + 64;
 }
@@ -713,14 +744,26 @@ int launch(Params &P, cudaStream_t s) {
   static const bool fused_finish = getenv("KVC_K1_FUSED_FINISH") != nullptr;
   P.fuse_finish = fused_finish ? 1 : 0;
   if (!P.counter_ready) cudaMemsetAsync(P.counter, 0, (1 + P.batch * P.p.num_kv_heads) * sizeof(int), s);
-  fa<<<grid, kThreads, smem, s>>>(tmK, tmV, P);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_off() ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, fa, tmK, tmV, P);
+  }
   if (!P.fuse_finish) {
     const int smem_b = (2 + P.n_ck) * kHP * 4;
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
-    fb<<<P.batch * P.p.num_kv_heads, 256, smem_b, s>>>(P);
+    launch_pdl(fb, P.batch * P.p.num_kv_heads, 256, smem_b, s, P);
   }
   const int pairs = P.batch * P.p.num_kv_heads;
-  k_decode_bump<<<(pairs + 255) / 256, 256, 0, s>>>(P);
+  launch_pdl(k_decode_bump, (pairs + 255) / 256, 256, 0, s, P);
   return cudaGetLastError() == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
 }
 
@@ -772,9 +815,11 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.n_items = P.n_ck * a->batch * H;
   P.scale = 1.4426950408889634f / sqrtf((float)D);
   char *base = reinterpret_cast<char *>(pool->scratch);
-  P.counter = reinterpret_cast<int *>(base);  // work-queue head + per-pair counters, zeroed per launch
+  // work-queue head + per-pair counters: the caller's persistent zeroed
+  // array (left zero by k_decode_bump), else a scratch copy zeroed per launch
+  P.counter = a->queue ? a->queue : reinterpret_cast<int *>(base);
   P.pair_done = P.counter + 1;
-  P.counter_ready = 0;
+  P.counter_ready = a->queue ? 1 : 0;
   int64_t off = ((int64_t)(1 + a->batch * H) * 4 + 255) / 256 * 256;
   P.scores = reinterpret_cast<float *>(base + off);
   off += (int64_t)a->batch * H * P.max_ctx_pad * r * 4;
