@@ -222,6 +222,19 @@ def populate(S, args):
         row = tables.row(s)
         tables.ctx[row] = ctx
         tables.ctx_bound[row] = int(ctx.max())
+    # per-slot metadata (metric, logical, protected) copied block by block
+    # from the template head, so the copies are valid compress() inputs
+    store, b = S["store"], S["b"]
+    mt, lg, pr = store.metrics.view(-1), store.logical.view(-1), store.protected_u8.view(-1)
+    off = torch.arange(b, device=tables.tables.device, dtype=torch.int64)
+    jj = torch.arange(tables.max_blocks, device=tables.tables.device)
+    for s in range(P, S["B"]):
+        t = s % P
+        nb = tables.nblocks[tables.row(t)]
+        live = (jj[None, None, :] < nb[..., None].long())
+        src = (tables.tables[tables.row(t)].long()[live][:, None] * b + off).reshape(-1)
+        dst = (tables.tables[tables.row(s)].long()[live][:, None] * b + off).reshape(-1)
+        mt[dst], lg[dst], pr[dst] = mt[src], lg[src], pr[src]
     # fill every pool block with unit-normal bf16 (K/V of the copied heads)
     cache = S["cache"]
     kf, vf = cache.keys.view(-1), cache.values.view(-1)
@@ -322,12 +335,48 @@ def decode_bench(S, args, e2e=False):
         res["k1_bytes_mean"] = float(bytes_steps.mean())
         res["k1_gbs"] = float(bytes_steps.sum() / (durs.sum() * 1e-3) / 1e9)
         res["bytes_per_step"] = float(bytes_steps.sum(axis=1).mean())
-        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream + finish) + fresh clear
-        res["launches_per_step"] = 4 + 2 * l + 1
+        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream, finish, bump) + fresh clear
+        res["launches_per_step"] = 4 + 3 * l + 1
     else:
         res["h2d"] = int(sum(x.numel() * 2 for x in (hq[0], hk[0], hv[0])))
         res["d2h"] = int(hout.numel() * 2)
     return res
+
+
+def decode_compression_rounds(S, args, rounds=2, gap_steps=8):
+    """The engine's every-step policy (engine.py:89-93, 275-280, 360-378):
+    one compress() over the whole running batch, budgets from
+    budget_to_blocks(prompt_len / rate), metric from decode accumulation.
+    `gap_steps` decode steps between rounds give every head new tokens.
+    Returns per-round device ms of K3+K4 and the blocks each freed."""
+    torch, K = S["torch"], S["K"]
+    cache, tables, manager, store, cfg = S["cache"], S["tables"], S["manager"], S["store"], S["cfg"]
+    dev = cache.device
+    B, l, H, n_q, d, b = S["B"], S["l"], S["H"], S["n_q"], S["d"], S["b"]
+    seqs = list(range(B))
+    rows = [tables.row(s) for s in seqs]
+    rows_t = torch.tensor(rows, dtype=torch.int32, device=dev)
+    q = torch.randn((B, n_q, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+    kv = torch.randn((B, H, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+    out = {"ms": [], "freed": [], "sequences": B}
+    for _ in range(rounds):
+        for _ in range(gap_steps):
+            manager.allocate_decode_step(seqs, sync=False)
+            for m in range(l):
+                K.paged_decode(q, cache, tables, None, m, cfg, store=store, metric_mode=2, k_new=kv, v_new=kv,
+                               fresh=True, rows_tensor=rows_t, host_rows=rows)
+            _clear_fresh_rows(S, rows_t)
+        nb = tables.nblocks[rows_t.long()].reshape(B, -1).sum(dim=1).tolist()
+        budgets = {s: K.budget_to_blocks(S["keep_tokens"], l, H, b, int(nb[i])) for i, s in enumerate(seqs)}
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        plan = K.compress(cache, tables, manager, store, budgets, sync=False, events=(e0, e1))
+        torch.cuda.synchronize()
+        S["_lib"].DeviceContext.get(dev).raise_status()
+        K.compression.refresh_ctx_bounds(tables, seqs)
+        out["ms"].append(e0.elapsed_time(e1))
+        out["freed"].append(int(plan.totals.tolist()[0]))
+    return out
 
 
 def _clear_fresh_rows(S, rows_t):
@@ -488,6 +537,7 @@ def main():
         gather_round_counts(S["manager"], [sum(ev["freed"]), sum(ev["evicted"]), sum(ev["moves"])])
     dec = decode_bench(S, args)
     e2e = None if args.no_e2e else decode_bench(S, args, e2e=True)
+    dcr = decode_compression_rounds(S, args)
     ms = dec["ms"]
     ms_e2e = e2e["ms"] if e2e else None
     if dist is not None:
@@ -514,6 +564,11 @@ def main():
         "ratio_to_decode_step": {
             "raw_with_k2": ((k2 or 0) + (k34 or 0)) / step_ms, "raw_without_k2": (k34 or 0) / step_ms,
             "amortised_500_tokens_with_k2": ((k2 or 0) + (k34 or 0)) * B / 500 / step_ms},
+        "decode_round": {
+            "what": f"every-step policy: one compress() over all {B} running sequences "
+                    f"(K3+K4, decode-accumulated L2 metric), {8} decode steps after the previous round",
+            "ms": dcr["ms"], "freed_blocks": dcr["freed"],
+            "ratio_to_decode_step": dcr["ms"][-1] / step_ms},
     }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,

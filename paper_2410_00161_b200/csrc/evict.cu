@@ -50,6 +50,7 @@ struct EvictState {
   int32_t *R;         // [n_seqs][kBins] contribution deltas per digit
   uint32_t *prefix;   // [n_seqs] T* digits found so far
   int64_t *E;         // [n_seqs] clamped budget (0 = inactive)
+  int64_t *seq_moves; // [n_seqs] move slots of the sequence, then its base offset
   int64_t max_slots;
   int hp;
   int32_t *status;
@@ -70,12 +71,13 @@ __device__ __forceinline__ void hist_add(int32_t *hist, uint32_t bin, bool activ
   if ((threadIdx.x & 31) == leader) atomicAdd(&hist[bin], __popc(peers));
 }
 
-// Per-head inclusive scan of a kBins histogram in smem (kThreads threads,
+// Per-head inclusive scan of a kBins histogram in smem (NT threads,
 // 4 bins each).  Writes the inclusive cumulative counts back into hist.
+template <int NT>
 __device__ void scan_hist(int32_t *hist) {
-  using Scan = cub::BlockScan<int32_t, kThreads>;
+  using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
-  constexpr int per = kBins / kThreads;
+  constexpr int per = kBins / NT;
   int32_t v[per];
   int32_t s = 0;
 #pragma unroll
@@ -95,8 +97,9 @@ __device__ void scan_hist(int32_t *hist) {
 }
 
 // Add this head's contribution deltas min(cap, floor((base+cum[c])/b)) to R.
+template <int NT>
 __device__ void add_contrib(const int32_t *cum, int64_t base, int cap, int b, int32_t *R, int nbins) {
-  for (int c = threadIdx.x; c < nbins; c += kThreads) {
+  for (int c = threadIdx.x; c < nbins; c += NT) {
     // delta form: bin 0 carries the absolute value, later bins the increase
     int64_t z = (base + cum[c]) / b;
     if (z > cap) z = cap;
@@ -110,7 +113,8 @@ __device__ void add_contrib(const int32_t *cum, int64_t base, int cap, int b, in
 }
 
 // (1) keys + cap + level-1 histogram contributions.
-__global__ void __launch_bounds__(kThreads) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
                                                   EvictState S, int with_hist) {
   __shared__ int32_t hist[kBins];
   __shared__ int32_t shield_s;
@@ -127,13 +131,13 @@ __global__ void __launch_bounds__(kThreads) k_load(kvc_pool p, const int32_t *ro
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_CAPACITY, (int32_t)hidx, (int32_t)n);
     return;
   }
-  for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+  for (int i = threadIdx.x; i < kBins; i += NT) hist[i] = 0;
   if (threadIdx.x == 0) shield_s = 0;
   __syncthreads();
   int shield = 0;
   if (b == 16) {
     // one thread per 16-slot block: 64 B metric, 16 B flags, 64 B keys
-    for (int64_t base = 0; base < nb; base += kThreads) {
+    for (int64_t base = 0; base < nb; base += NT) {
       const int64_t bl = base + threadIdx.x;
       const bool in = bl < nb;
       uint32_t kk[16];
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) k_load(kvc_pool p, const int32_t *ro
       }
     }
   } else {
-    for (int64_t base = 0; base < n; base += kThreads) {
+    for (int64_t base = 0; base < n; base += NT) {
       const int64_t pos = base + threadIdx.x;
       const bool in = pos < n;
       uint32_t key = 0;
@@ -188,8 +192,8 @@ __global__ void __launch_bounds__(kThreads) k_load(kvc_pool p, const int32_t *ro
   if (cap < 0) cap = 0;
   if (threadIdx.x == 0) S.cap[g] = cap;
   if (!with_hist || req[si] <= 0) return;
-  scan_hist(hist);
-  add_contrib(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
+  scan_hist<NT>(hist);
+  add_contrib<NT>(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
 }
 
 // (2/4/6) per sequence: clamp E, find the first digit whose cumulative row
@@ -255,7 +259,8 @@ __global__ void __launch_bounds__(1024) k_find(const int64_t *req, EvictState S,
 }
 
 // (3/5) per head: histogram of the next digit among keys matching the prefix.
-__global__ void __launch_bounds__(kThreads) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
                                                   int shift, int bits) {
   __shared__ int32_t hist[kBins];
   __shared__ int64_t below_s;
@@ -268,11 +273,11 @@ __global__ void __launch_bounds__(kThreads) k_hist(kvc_pool p, const int32_t *ro
   const uint32_t pre = S.prefix[si];
   const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
   const uint32_t dmask = (1u << bits) - 1;
-  for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+  for (int i = threadIdx.x; i < kBins; i += NT) hist[i] = 0;
   if (threadIdx.x == 0) below_s = 0;
   __syncthreads();
   int32_t below = 0;
-  for (int64_t base = 0; base < n; base += 4 * kThreads) {
+  for (int64_t base = 0; base < n; base += 4 * NT) {
     const int64_t pos = base + 4 * threadIdx.x;  // max_slots is a multiple of 4
     uint4 k4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
     if (pos < n) k4 = *reinterpret_cast<const uint4 *>(keys + pos);
@@ -287,13 +292,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(kvc_pool p, const int32_t *ro
   }
   atomicAdd((unsigned long long *)&below_s, (unsigned long long)below);
   __syncthreads();
-  scan_hist(hist);
-  add_contrib(hist, below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
+  scan_hist<NT>(hist);
+  add_contrib<NT>(hist, below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
 }
 
 // (7) per head: rows with threshold < T* and <= T*.
-__global__ void __launch_bounds__(kThreads) k_bounds(kvc_pool p, const int32_t *rows, EvictState S) {
-  using Red = cub::BlockReduce<int32_t, kThreads>;
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, EvictState S) {
+  using Red = cub::BlockReduce<int32_t, NT>;
   __shared__ typename Red::TempStorage tmp;
   const int g = blockIdx.x;
   const int si = g / S.hp, hi = g % S.hp;
@@ -307,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(kvc_pool p, const int32_t *
   const uint32_t T = S.prefix[si];
   const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
   int32_t lt = 0, le = 0;
-  for (int64_t pos = threadIdx.x; pos < n; pos += kThreads) {
+  for (int64_t pos = threadIdx.x; pos < n; pos += NT) {
     const uint32_t k = keys[pos];
     lt += k < T;
     le += k <= T;
@@ -324,59 +330,73 @@ __global__ void __launch_bounds__(kThreads) k_bounds(kvc_pool p, const int32_t *
   }
 }
 
-// (8) one CTA: per sequence e_h = L_h + ties taken in head order; global
-// exclusive offsets of e_h*b for the move lists.
-__global__ void __launch_bounds__(1024) k_select(EvictState S, int n_seqs, int bsz, int32_t *evict,
-                                                int64_t *move_off, int32_t *status) {
+// (8) one CTA per sequence: e_h = L_h + ties taken in head order, and the
+// sequence-local exclusive offsets of e_h*b (made global by k_offsets).
+__global__ void __launch_bounds__(1024) k_select(EvictState S, int bsz, int32_t *evict, int64_t *move_off,
+                                                int32_t *status) {
   using Scan = cub::BlockScan<int64_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
-  __shared__ int64_t carry, less_s;
+  __shared__ int64_t less_s;
   const int hp = S.hp;
+  const int si = blockIdx.x;
+  const int64_t E = S.E[si];
+  // total rows strictly below T*
+  if (threadIdx.x == 0) less_s = 0;
+  __syncthreads();
+  int64_t less = 0;
+  for (int h = threadIdx.x; h < hp; h += 1024) less += E > 0 ? S.lo[(int64_t)si * hp + h] : 0;
+  atomicAdd((unsigned long long *)&less_s, (unsigned long long)less);
+  __syncthreads();
+  const int64_t need = E - less_s;  // tie rows to take at T*, in head order
+  int64_t tcarry = 0, ocarry = 0;
+  for (int base = 0; base < hp; base += 1024) {
+    const int h = base + threadIdx.x;
+    const int64_t g = (int64_t)si * hp + h;
+    int64_t ties = 0;
+    if (h < hp && E > 0) ties = S.hi[g] - S.lo[g];
+    int64_t excl, tot;
+    Scan(tmp).ExclusiveSum(ties, excl, tot);
+    int32_t eh = 0;
+    if (h < hp) {
+      int64_t take = need - (tcarry + excl);
+      if (take < 0) take = 0;
+      if (take > ties) take = ties;
+      eh = E > 0 ? (int32_t)(S.lo[g] + take) : 0;
+      evict[g] = eh;
+    }
+    __syncthreads();
+    int64_t oex, otot;
+    Scan(tmp).ExclusiveSum((int64_t)eh * bsz, oex, otot);
+    if (h < hp) move_off[g] = ocarry + oex;
+    __syncthreads();
+    tcarry += tot;
+    ocarry += otot;
+  }
+  if (threadIdx.x == 0) {
+    S.seq_moves[si] = ocarry;
+    if (E > 0 && (need < 0 || need > tcarry)) set_status(status, KVC_DEV_SCHEDULE_CORRUPTION, si, (int32_t)need);
+  }
+}
+
+// (8b) one CTA: sequence bases -> global exclusive offsets over all heads.
+__global__ void __launch_bounds__(1024) k_offsets(EvictState S, int n_seqs, int64_t *move_off) {
+  using Scan = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int si = 0; si < n_seqs; ++si) {
-    const int64_t E = S.E[si];
-    // total rows strictly below T*
-    if (threadIdx.x == 0) less_s = 0;
-    __syncthreads();
-    int64_t less = 0;
-    for (int h = threadIdx.x; h < hp; h += 1024) less += E > 0 ? S.lo[(int64_t)si * hp + h] : 0;
-    atomicAdd((unsigned long long *)&less_s, (unsigned long long)less);
-    __syncthreads();
-    const int64_t need = E - less_s;  // tie rows to take at T*, in head order
-    int64_t tcarry = 0;
-    for (int base = 0; base < hp; base += 1024) {
-      const int h = base + threadIdx.x;
-      const int64_t g = (int64_t)si * hp + h;
-      int64_t ties = 0;
-      if (h < hp && E > 0) ties = S.hi[g] - S.lo[g];
-      int64_t excl, tot;
-      Scan(tmp).ExclusiveSum(ties, excl, tot);
-      if (h < hp) {
-        int64_t take = need - (tcarry + excl);
-        if (take < 0) take = 0;
-        if (take > ties) take = ties;
-        evict[g] = E > 0 ? (int32_t)(S.lo[g] + take) : 0;
-      }
-      __syncthreads();
-      tcarry += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0 && E > 0 && (need < 0 || need > tcarry)) set_status(status, KVC_DEV_SCHEDULE_CORRUPTION, si, (int32_t)need);
-    __syncthreads();
-  }
-  // exclusive offsets over all heads of e_h * b (move capacity per head)
-  const int64_t T = (int64_t)n_seqs * hp;
-  for (int64_t base = 0; base < T; base += 1024) {
-    const int64_t g = base + threadIdx.x;
-    int64_t v = g < T ? (int64_t)evict[g] * bsz : 0;
+  for (int base = 0; base < n_seqs; base += 1024) {
+    const int si = base + threadIdx.x;
+    const int64_t v = si < n_seqs ? S.seq_moves[si] : 0;
     int64_t excl, tot;
     Scan(tmp).ExclusiveSum(v, excl, tot);
-    if (g < T) move_off[g] = carry + excl;
+    if (si < n_seqs) S.seq_moves[si] = carry + excl;  // now the sequence base
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
+  const int64_t T = (int64_t)n_seqs * S.hp;
+  for (int64_t g = threadIdx.x; g < T; g += 1024) move_off[g] += S.seq_moves[g / S.hp];
   if (threadIdx.x == 0) move_off[T] = carry;
 }
 
@@ -405,7 +425,7 @@ __device__ uint32_t cta_select(int32_t *hist, int64_t n, int64_t rank, GetV getv
       hist_add(hist, (v >> shift) & dmask, match);
     }
     __syncthreads();
-    scan_hist(hist);  // inclusive
+    scan_hist<kThreads>(hist);  // inclusive
     for (int c = threadIdx.x; c < (1 << bits); c += kThreads) {
       const int64_t excl = c > 0 ? hist[c - 1] : 0;
       if (excl <= rank && rank < hist[c]) {
@@ -611,12 +631,12 @@ __global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t 
 // 16-slot block in every pass (uint4 key / int4 logical rows).
 // ---------------------------------------------------------------------------
 
-constexpr int kT16 = 1024;
 
-__device__ void scan_hist16(int32_t *hist) {  // inclusive, kT16 threads
-  using Scan = cub::BlockScan<int32_t, kT16>;
+template <int NT>
+__device__ void scan_hist16(int32_t *hist) {  // inclusive, NT threads
+  using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
-  constexpr int per = kBins / kT16;
+  constexpr int per = kBins / NT;
   int32_t v[per];
   int32_t s = 0;
 #pragma unroll
@@ -638,7 +658,7 @@ __device__ void scan_hist16(int32_t *hist) {  // inclusive, kT16 threads
 // rank-th smallest value among the positions `get4` marks valid, 4 per call.
 // Returns the value; *rank_out = its rank among equal values, *eq_out = how
 // many valid positions hold it.
-template <typename Get4>
+template <int NT, typename Get4>
 __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, int64_t *rank_out,
                              int64_t *eq_out) {
   __shared__ uint32_t pre_s;
@@ -651,9 +671,9 @@ __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, 
     const int shift = shifts[lv], bits = bitsv[lv];
     const int shift_hi = shift + bits;
     const uint32_t dmask = (1u << bits) - 1;
-    for (int i = threadIdx.x; i < kBins; i += kT16) hist[i] = 0;
+    for (int i = threadIdx.x; i < kBins; i += NT) hist[i] = 0;
     __syncthreads();
-    for (int64_t qb = 0; qb * 4 < n; qb += kT16) {  // warp-uniform trip count (hist_add votes)
+    for (int64_t qb = 0; qb * 4 < n; qb += NT) {  // warp-uniform trip count (hist_add votes)
       const int64_t q = qb + threadIdx.x;
       uint32_t v[4] = {0u, 0u, 0u, 0u};
       bool ok[4] = {false, false, false, false};
@@ -665,8 +685,8 @@ __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, 
       }
     }
     __syncthreads();
-    scan_hist16(hist);
-    for (int c = threadIdx.x; c < (1 << bits); c += kT16) {
+    scan_hist16<NT>(hist);
+    for (int c = threadIdx.x; c < (1 << bits); c += NT) {
       const int64_t excl = c > 0 ? hist[c - 1] : 0;
       if (excl <= rank && rank < hist[c]) {
         pre_s = (pre << bits) | (uint32_t)c;
@@ -685,11 +705,12 @@ __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, 
   return pre;
 }
 
-__global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
   extern __shared__ uint32_t bitmap[];  // [words] bitmap + [words] prefix
   __shared__ int32_t hist[kBins];
   __shared__ int32_t cnt_s[4];
-  using Scan = cub::BlockScan<int32_t, kT16>;
+  using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage stmp;
   const int g = blockIdx.x;
   const int si = g / S.hp, hi = g % S.hp;
@@ -715,7 +736,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
     tie_rank = target - lt;
     tie_cnt = le - lt;
   } else {
-    T = select16(hist, n, target, [&](int64_t pos, uint32_t *v, bool *ok) {
+    T = select16<NT>(hist, n, target, [&](int64_t pos, uint32_t *v, bool *ok) {
       const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
       v[0] = k4.x; v[1] = k4.y; v[2] = k4.z; v[3] = k4.w;
 #pragma unroll
@@ -729,7 +750,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
   uint32_t Sx = 0xffffffffu;
   if (tie_rank + 1 < tie_cnt) {
     int64_t dummy, dummy2;
-    Sx = select16(hist, n, tie_rank, [&](int64_t pos, uint32_t *v, bool *ok) {
+    Sx = select16<NT>(hist, n, tie_rank, [&](int64_t pos, uint32_t *v, bool *ok) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int64_t ps = pos + i;
@@ -770,7 +791,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
   };
   {
     int32_t carry = 0;
-    for (int base = 0; base < rb; base += kT16) {
+    for (int base = 0; base < rb; base += NT) {
       const int bl = base + threadIdx.x;
       uint32_t holes = 0;
       int64_t f0 = 0;
@@ -799,7 +820,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
   }
   {
     int32_t carry = 0;
-    for (int base = 0; base < e; base += kT16) {
+    for (int base = 0; base < e; base += NT) {
       const int t = base + threadIdx.x;
       const int bl = nb - 1 - t;  // descending blocks
       uint32_t surv = 0;
@@ -834,7 +855,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
     return;
   }
-  for (int k = threadIdx.x; k < nmoves; k += kT16) {
+  for (int k = threadIdx.x; k < nmoves; k += NT) {
     const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
     p.metric[dst] = p.metric[src];
     p.logical[dst] = p.logical[src];
@@ -843,7 +864,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
   }
   __syncthreads();
   // ---- free the trailing e blocks and reset their slots ----
-  for (int t = threadIdx.x; t < e; t += kT16) {
+  for (int t = threadIdx.x; t < e; t += NT) {
     const int j = rb + t;
     const int32_t blk = tab[j];
     const int64_t f0 = (int64_t)blk * 16;
@@ -865,10 +886,10 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
   // ---- logical renumbering: rank among the kept logicals ----
   const int words = (int)((n + 31) / 32);
   uint32_t *wpre = bitmap + words;
-  for (int w = threadIdx.x; w < words; w += kT16) bitmap[w] = 0;
+  for (int w = threadIdx.x; w < words; w += NT) bitmap[w] = 0;
   __syncthreads();
   const int kb = (Cn + 15) / 16;
-  for (int bl = threadIdx.x; bl < kb; bl += kT16) {
+  for (int bl = threadIdx.x; bl < kb; bl += NT) {
     const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -891,7 +912,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
   __syncthreads();
   {
     int32_t carry = 0;
-    for (int base = 0; base < words; base += kT16) {
+    for (int base = 0; base < words; base += NT) {
       const int w = base + threadIdx.x;
       const int32_t c = w < words ? __popc(bitmap[w]) : 0;
       int32_t excl, tot;
@@ -902,7 +923,7 @@ __global__ void __launch_bounds__(kT16) k_compact16(kvc_pool p, const int32_t *r
     }
   }
   __syncthreads();
-  for (int bl = threadIdx.x; bl < kb; bl += kT16) {
+  for (int bl = threadIdx.x; bl < kb; bl += NT) {
     int4 *lp = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1027,7 +1048,9 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.R = sc.take<int32_t>((int64_t)a->n_seqs * kBins);
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
-  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.prefix || !S.E) return KVC_ERR_INVALID;
+  S.seq_moves = sc.take<int64_t>(a->n_seqs);
+  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.prefix || !S.E || !S.seq_moves)
+    return KVC_ERR_INVALID;
   return KVC_OK;
 }
 
@@ -1039,17 +1062,37 @@ int validate(const kvc_pool *pool, const kvc_evict_args *a) {
   return KVC_OK;
 }
 
+// Threads per head for the histogram passes and the compaction: heads of at
+// most 8192 slots (the decode-time batch) use small CTAs so more heads are
+// resident at once; long prefill heads use wide ones.
+static bool small_heads(const EvictState &S) { return S.max_slots <= 8192; }
+
 int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
   const int64_t T = (int64_t)a->n_seqs * S.hp;
   cudaMemsetAsync(S.R, 0, (int64_t)a->n_seqs * kBins * sizeof(int32_t), s);
-  k_load<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1);
-  k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 1, 11, a->clamped);
-  k_hist<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11);
-  k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 2, 11, a->clamped);
-  k_hist<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10);
-  k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 3, 10, a->clamped);
-  k_bounds<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, S);
-  k_select<<<1, 1024, 0, s>>>(S, a->n_seqs, pool->block_size, a->evict, a->move_offsets, pool->status);
+  if (small_heads(S)) {
+    constexpr int NT = 256;
+    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1);
+    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 1, 11, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11);
+    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 2, 11, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10);
+    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 3, 10, a->clamped);
+    k_bounds<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S);
+  } else {
+    constexpr int NT = kThreads;
+    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1);
+    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 1, 11, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11);
+    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 2, 11, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10);
+    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 3, 10, a->clamped);
+    k_bounds<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S);
+  }
+  if (a->n_seqs > 0) {
+    k_select<<<a->n_seqs, 1024, 0, s>>>(S, pool->block_size, a->evict, a->move_offsets, pool->status);
+    k_offsets<<<1, 1024, 0, s>>>(S, a->n_seqs, a->move_offsets);
+  }
   KVC_CHECK_LAUNCH();
   return KVC_OK;
 }
@@ -1069,10 +1112,12 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
   if (pool->block_size == 16) {
     static bool conf16 = false;
     if (!conf16) {
-      cudaFuncSetAttribute(k_compact16, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_compact16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_compact16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       conf16 = true;
     }
-    k_compact16<<<(int)T, kT16, dyn, s>>>(*pool, a->seq_rows, S, M);
+    if (small_heads(S)) k_compact16<256><<<(int)T, 256, dyn, s>>>(*pool, a->seq_rows, S, M);
+    else k_compact16<1024><<<(int)T, 1024, dyn, s>>>(*pool, a->seq_rows, S, M);
   } else {
     k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
   }
@@ -1105,7 +1150,8 @@ int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *a, void *strea
   cudaStream_t s = (cudaStream_t)stream;
   // keys are recomputed so the call is self-contained
   const int64_t T = (int64_t)a->n_seqs * S.hp;
-  k_load<<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0);
+  if (small_heads(S)) k_load<256><<<(int)T, 256, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0);
+  else k_load<kThreads><<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0);
   return run_compact(pool, a, S, s);
 }
 

@@ -176,6 +176,33 @@ def test_llama_slice_exact():
     assert got["freed_blocks"] == E
 
 
+@pytest.mark.parametrize("L,E_div", [(12000, 8), (9000, 3)])
+def test_long_heads_exact(L, E_div):
+    """Heads longer than 8192 slots take the wide-CTA kernels (prefill-sized
+    heads); shorter ones the 256-thread kernels every other test covers."""
+    rng = np.random.default_rng(L)
+    b, d, layers, heads = 16, 64, 1, 3
+    nblocks = layers * heads * (-(-L // b)) + 64
+    st = O.OracleState(nblocks, b, d, layers, heads)
+    O.alloc_prefill(st, 0, L)
+    for h in range(heads):
+        C = L - 37 * h
+        st.ctx[0][0, h] = C
+        f = st.live_slots(0, 0, h)
+        st.keys[f] = bf16_round(rng.standard_normal((C, d)))
+        st.values[f] = bf16_round(rng.standard_normal((C, d)))
+        st.metric[f] = f32_round(O.pool_max((rng.random(C) ** 2)[None], 7)[0])
+        st.logical[f] = np.arange(C)
+        st.protected[f[-8:]] = True
+    rig = DevRig(nblocks, b, d, layers, heads, max_seqs=2)
+    rig.load(st)
+    E = st.block_count(0) // E_div
+    got = device_compress(rig, {0: E})
+    want = O.compress(st, {0: E})
+    assert got == want
+    assert_state_equal(rig, st)
+
+
 def test_totals_and_free_count():
     rng = np.random.default_rng(3)
     st = fuzz_state(rng, 4, 8, 1, 3, [1, 2], 40, "iid")
