@@ -62,13 +62,10 @@ __device__ __forceinline__ uint32_t slot_key(const kvc_pool &p, int64_t f, bool 
   return f32_order_key(p.metric[f]);
 }
 
-// Warp-aggregated shared-memory histogram increment.
+// Shared-memory histogram increment (same-bin lanes serialise in hardware;
+// warp aggregation with match.any measured slower for metric keys).
 __device__ __forceinline__ void hist_add(int32_t *hist, uint32_t bin, bool active) {
-  const unsigned mask = __ballot_sync(0xffffffffu, active);
-  if (!active) return;
-  const unsigned peers = __match_any_sync(mask, bin);
-  const int leader = __ffs(peers) - 1;
-  if ((threadIdx.x & 31) == leader) atomicAdd(&hist[bin], __popc(peers));
+  if (active) atomicAdd(&hist[bin], 1);
 }
 
 // Per-head inclusive scan of a kBins histogram in smem (NT threads,
@@ -96,19 +93,20 @@ __device__ void scan_hist(int32_t *hist) {
   __syncthreads();
 }
 
-// Add this head's contribution deltas min(cap, floor((base+cum[c])/b)) to R.
+// Add this head's contribution deltas min(cap, floor((base+cum[c])/b)) to R
+// (counts are < 2^31: one head's slots).
 template <int NT>
-__device__ void add_contrib(const int32_t *cum, int64_t base, int cap, int b, int32_t *R, int nbins) {
+__device__ void add_contrib(const int32_t *cum, int32_t base, int cap, int b, int32_t *R, int nbins) {
   for (int c = threadIdx.x; c < nbins; c += NT) {
     // delta form: bin 0 carries the absolute value, later bins the increase
-    int64_t z = (base + cum[c]) / b;
+    int32_t z = (base + cum[c]) / b;
     if (z > cap) z = cap;
-    int64_t a = 0;
+    int32_t a = 0;
     if (c > 0) {
       a = (base + cum[c - 1]) / b;
       if (a > cap) a = cap;
     }
-    if (z > a) atomicAdd(&R[c], (int32_t)(z - a));
+    if (z > a) atomicAdd(&R[c], z - a);
   }
 }
 
@@ -185,7 +183,8 @@ __global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, co
       if (with_hist) hist_add(hist, key >> 21, in);
     }
   }
-  atomicAdd(&shield_s, shield);
+  shield = __reduce_add_sync(0xffffffffu, shield);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&shield_s, shield);
   __syncthreads();
   const int sh_blocks = (shield_s + b - 1) / b;
   int cap = nb - (sh_blocks > 1 ? sh_blocks : 1);
@@ -290,10 +289,11 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
       hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
     }
   }
-  atomicAdd((unsigned long long *)&below_s, (unsigned long long)below);
+  below = __reduce_add_sync(0xffffffffu, below);
+  if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)&below_s, (unsigned long long)below);
   __syncthreads();
   scan_hist<NT>(hist);
-  add_contrib<NT>(hist, below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
+  add_contrib<NT>(hist, (int32_t)below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
 }
 
 // (7) per head: rows with threshold < T* and <= T*.
@@ -952,11 +952,794 @@ __global__ void __launch_bounds__(NT) k_compact16(kvc_pool p, const int32_t *row
   }
 }
 
-// K/V rows of every move of the round: grid (head, part); a warp moves one
+// ---------------------------------------------------------------------------
+// k_compact_smem: k_compact16 for heads of at most 8192 slots (the
+// decode-time batch).  The head's keys and logicals are staged in shared
+// memory once; both radix selects (8-bit digits, 4 levels) and the logical
+// renumbering run there, so the CTA's dependent global round trips are the
+// stage-in, the move/free metadata writes and the logical write-back.
+// Same pairing and renumbering as k_compact16 (compression.py:234-309).
+// ---------------------------------------------------------------------------
+
+// rank-th smallest (0-based) of getv over [0, n) (valid entries only); also
+// its rank among equal values and their count.  hist: 256 ints of smem.
+template <int NT, typename GetV>
+__device__ uint32_t smem_select(int32_t *hist, int n, int64_t rank, GetV getv, int64_t *rank_out, int64_t *eq_out) {
+  using Scan = cub::BlockScan<int32_t, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t pre_s;
+  __shared__ int64_t rank_s, eq_s;
+  static_assert(NT >= 256, "one bin per thread");
+  uint32_t pre = 0;
+  int64_t eq = 0;
+  for (int lv = 0; lv < 4; ++lv) {
+    const int shift = 24 - 8 * lv;
+    if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) {
+      uint32_t v;
+      if (getv(i, v) && (lv == 0 || (v >> (shift + 8)) == pre)) atomicAdd(&hist[(v >> shift) & 255], 1);
+    }
+    __syncthreads();
+    const int32_t h = threadIdx.x < 256 ? hist[threadIdx.x] : 0;
+    int32_t excl;
+    Scan(tmp).ExclusiveSum(h, excl);
+    if (threadIdx.x < 256 && excl <= rank && rank < excl + h) {
+      pre_s = (pre << 8) | threadIdx.x;
+      rank_s = rank - excl;
+      eq_s = h;
+    }
+    __syncthreads();
+    pre = pre_s;
+    rank = rank_s;
+    eq = eq_s;
+  }
+  *rank_out = rank;
+  *eq_out = eq;
+  return pre;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_compact_smem(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
+  extern __shared__ __align__(16) uint32_t dyn[];
+  __shared__ int32_t hist[256];
+  __shared__ int32_t cnt_s[4];
+  using Scan = cub::BlockScan<int32_t, NT>;
+  __shared__ typename Scan::TempStorage stmp;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  const int e = M.evict[g];
+  if (threadIdx.x == 0 && M.move_counts) M.move_counts[g] = 0;
+  if (threadIdx.x == 0 && M.evicted_kvs) M.evicted_kvs[g] = 0;
+  if (e <= 0) return;
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int nb = p.nblocks[hidx];
+  const int C = p.ctx[hidx];
+  const int n = nb * 16;
+  const int32_t *tab = head_table(p, hidx);
+  const int ms = (int)S.max_slots;
+  uint32_t *keys = dyn;                                     // [ms]
+  int32_t *lgs = reinterpret_cast<int32_t *>(dyn + ms);     // [ms] logical by position
+  uint32_t *bitmap = dyn + 2 * ms;                          // [ms/32]
+  int32_t *wpre = reinterpret_cast<int32_t *>(bitmap + (ms + 31) / 32);
+  // ---- stage keys and logicals by position ----
+  const uint32_t *gk = S.keys + (int64_t)g * S.max_slots;
+  for (int bl = threadIdx.x; bl < nb; bl += NT) {
+    const uint4 *kp = reinterpret_cast<const uint4 *>(gk + bl * 16);
+    const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
+    uint4 *ks = reinterpret_cast<uint4 *>(keys + bl * 16);
+    int4 *ls = reinterpret_cast<int4 *>(lgs + bl * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ks[q] = kp[q];
+      ls[q] = lp[q];
+    }
+  }
+  __syncthreads();
+  // ---- threshold T_h = (16 e)-th smallest key; shortcut when it is T* ----
+  const uint32_t Tstar = S.prefix[si];
+  const int64_t lt = S.ltc[g], le = S.lec[g];
+  const int64_t target = (int64_t)16 * e - 1;
+  uint32_t T;
+  int64_t tie_rank, tie_cnt;
+  if (target >= lt) {
+    T = Tstar;
+    tie_rank = target - lt;
+    tie_cnt = le - lt;
+  } else {
+    T = smem_select<NT>(hist, n, target, [&](int i, uint32_t &v) { v = keys[i]; return v < Tstar; }, &tie_rank,
+                        &tie_cnt);
+  }
+  // ---- tie cut: ties at T ordered by (occupied, logical, position) ----
+  auto sec = [&](int pos, int32_t lg) -> uint32_t {
+    return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
+  };
+  uint32_t Sx = 0xffffffffu;
+  if (tie_rank + 1 < tie_cnt) {
+    int64_t d0, d1;
+    Sx = smem_select<NT>(hist, n, tie_rank, [&](int i, uint32_t &v) {
+      if (keys[i] != T) return false;
+      v = sec(i, lgs[i]);
+      return true;
+    }, &d0, &d1);
+  }
+  auto block_flags = [&](int bl, uint32_t &mb, uint32_t &lb) {
+    mb = 0;
+    lb = 0;
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const int pos = bl * 16 + o;
+      const uint32_t k = keys[pos];
+      const int32_t lg = lgs[pos];
+      const bool m = k < T || (k == T && (Sx == 0xffffffffu || sec(pos, lg) <= Sx));
+      mb |= (m ? 1u : 0u) << o;
+      lb |= (lg >= 0 ? 1u : 0u) << o;
+    }
+  };
+  auto occ_bits = [&](int bl) -> uint32_t {
+    const int occ_n = C - bl * 16;
+    return occ_n >= 16 ? 0xffffu : occ_n <= 0 ? 0u : ((1u << occ_n) - 1u);
+  };
+  // ---- MoveCache pairing: holes ascending below the range, survivors descending in it ----
+  const int rb = nb - e;
+  int32_t *mv = M.moves + M.move_off[g] * 2;
+  const int64_t cap_mv = (int64_t)16 * e;
+  // hole k's position is parked in keys[k]: k < #holes <= 16 rb, and the
+  // pass has finished reading keys below 16 (base + NT) when it writes them;
+  // the survivor pass reads only keys of the range (>= 16 rb)
+  int32_t *hole_pos = reinterpret_cast<int32_t *>(keys);
+  if (threadIdx.x == 0) { cnt_s[0] = 0; cnt_s[1] = 0; cnt_s[2] = 0; }
+  __syncthreads();
+  int32_t evk = 0;
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < rb; base += NT) {
+      const int bl = base + threadIdx.x;
+      uint32_t holes = 0;
+      if (bl < rb) {
+        uint32_t mb, lb;
+        block_flags(bl, mb, lb);
+        holes = (mb | ~lb) & 0xffffu;
+        evk += __popc(mb & occ_bits(bl));
+      }
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(__popc(holes), excl, tot);
+      int64_t k = carry + excl;
+      for (uint32_t hb = holes; hb; hb &= hb - 1) {
+        const int o = __ffs(hb) - 1;
+        if (k < cap_mv) {
+          mv[2 * k + 1] = tab[bl] * 16 + o;
+          hole_pos[k] = bl * 16 + o;
+        }
+        ++k;
+      }
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt_s[0] = carry;
+  }
+  __syncthreads();
+  int32_t nmoves;
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < e; base += NT) {
+      const int t = base + threadIdx.x;
+      const int bl = nb - 1 - t;
+      uint32_t surv = 0;
+      if (t < e) {
+        uint32_t mb, lb;
+        block_flags(bl, mb, lb);
+        surv = ~mb & lb & 0xffffu;
+        evk += __popc(mb & occ_bits(bl));
+      }
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(__popc(surv), excl, tot);
+      int64_t k = carry + excl;
+      const int64_t f0 = t < e ? (int64_t)tab[bl] * 16 : 0;
+      for (int o = 15; o >= 0; --o) {
+        if (surv >> o & 1u) {
+          if (k < cnt_s[0]) {
+            mv[2 * k] = (int32_t)(f0 + o);
+            hole_pos[k] |= (bl * 16 + o) << 16;  // pair k: hole position | survivor position << 16
+          }
+          ++k;
+        }
+      }
+      carry += tot;
+      __syncthreads();
+    }
+    nmoves = carry;
+  }
+  atomicAdd(&cnt_s[2], evk);
+  __syncthreads();
+  if (nmoves > cnt_s[0]) {
+    if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
+    return;
+  }
+  // metadata of every pair, one pair per thread (holes lie below the range,
+  // survivors inside it: no pair reads a slot another pair writes)
+  for (int k = threadIdx.x; k < nmoves; k += NT) {
+    const int hp_ = hole_pos[k] & 0xffff, sp_ = hole_pos[k] >> 16;
+    const int64_t dst = (int64_t)tab[hp_ >> 4] * 16 + (hp_ & 15);
+    const int64_t src = (int64_t)tab[sp_ >> 4] * 16 + (sp_ & 15);
+    p.metric[dst] = p.metric[src];
+    p.protected_[dst] = p.protected_[src];
+    p.fresh[dst] = p.fresh[src];
+    lgs[hp_] = lgs[sp_];
+  }
+  __syncthreads();
+  // ---- free the trailing e blocks and reset their slots ----
+  for (int t = threadIdx.x; t < e; t += NT) {
+    const int j = rb + t;
+    const int32_t blk = tab[j];
+    const int64_t f0 = (int64_t)blk * 16;
+    float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
+    int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      lp[q] = make_int4(-1, -1, -1, -1);
+    }
+    *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
+    p.free_flag[blk] = 1;
+    atomicAdd(&p.free_tile[blk / KVC_FREE_TILE], 1);
+    if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
+  }
+  const int keep = rb;
+  const int Cn = C < keep * 16 ? C : keep * 16;
+  // ---- logical renumbering: rank among the kept logicals ----
+  const int words = (n + 31) / 32;
+  for (int w = threadIdx.x; w < words; w += NT) bitmap[w] = 0;
+  __syncthreads();
+  for (int pos = threadIdx.x; pos < Cn; pos += NT) {
+    const int32_t lg = lgs[pos];
+    if (lg < 0 || lg >= n) {
+      set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+      continue;
+    }
+    const uint32_t bit = 1u << (lg & 31);
+    if (atomicOr(&bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+  }
+  __syncthreads();
+  {
+    int32_t carry = 0;
+    for (int base = 0; base < words; base += NT) {
+      const int w = base + threadIdx.x;
+      const int32_t c = w < words ? __popc(bitmap[w]) : 0;
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(c, excl, tot);
+      if (w < words) wpre[w] = carry + excl;
+      carry += tot;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  const int kb = (Cn + 15) / 16;
+  for (int bl = threadIdx.x; bl < kb; bl += NT) {
+    int4 *lp = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int32_t lv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pos = bl * 16 + q * 4 + i;
+        const int32_t lg = lgs[pos];
+        lv[i] = (pos >= Cn || lg < 0 || lg >= n) ? lg
+                : (int32_t)wpre[lg >> 5] + __popc(bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
+      }
+      lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    p.nblocks[hidx] = keep;
+    p.ctx[hidx] = Cn;
+    if (M.move_counts) M.move_counts[g] = nmoves;
+    if (M.evicted_kvs) M.evicted_kvs[g] = cnt_s[2];
+    if (M.totals) {
+      atomicAdd((unsigned long long *)&M.totals[0], (unsigned long long)e);
+      atomicAdd((unsigned long long *)&M.totals[1], (unsigned long long)cnt_s[2]);
+      atomicAdd((unsigned long long *)&M.totals[2], (unsigned long long)nmoves);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_compact_warp: one warp per head for heads of at most 8192 slots (the
+// decode-time batch: thousands of short heads, a few evicted blocks each).
+// No CTA barriers; 8 heads per CTA, 4 KB of shared memory per warp.
+//  * T_h and the tie cut come from the candidates (keys < T*, or the ties at
+//    T*) sorted by (key, secondary) in shared memory when there are at most
+//    kCand of them, else from a warp radix select over the head's keys.
+//  * holes / survivors / pairs / free / renumber as k_compact16, each pass
+//    one 16-slot block per lane with warp scans.
+// ---------------------------------------------------------------------------
+constexpr int kWC = 8;      // warps (heads) per CTA
+constexpr int kCand = 256;  // candidate capacity per warp
+
+struct WarpArea {
+  unsigned long long cand[kCand];  // composites (key << 32 | secondary); or a 256-bin histogram
+  uint32_t bitmap[256];            // kept-logical bitmap (n <= 8192)
+  int32_t wpre[256];               // its word prefix counts
+};
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int &total) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// rank-th smallest (0-based) of getv over positions [0, n); 8-bit digits.
+template <typename GetV>
+__device__ uint32_t warp_select(int32_t *hist, int n, int64_t rank, GetV getv, int lane, int64_t *rank_out,
+                                int64_t *eq_out) {
+  uint32_t pre = 0;
+  int64_t eq = 0;
+  for (int lv = 0; lv < 4; ++lv) {
+    const int shift = 24 - 8 * lv;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
+    for (int pos = lane; pos < n; pos += 32) {
+      uint32_t v;
+      if (getv(pos, v) && (lv == 0 || (v >> (shift + 8)) == pre)) atomicAdd(&hist[(v >> shift) & 255], 1);
+    }
+    __syncwarp();
+    int h[8], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      h[i] = hist[lane * 8 + i];
+      sum += h[i];
+    }
+    int tot;
+    int64_t run = warp_excl_scan(sum, lane, tot);
+    int found = -1;
+    int64_t frank = 0, feq = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (found < 0 && run <= rank && rank < run + h[i]) {
+        found = lane * 8 + i;
+        frank = rank - run;
+        feq = h[i];
+      }
+      run += h[i];
+    }
+    const unsigned fm = __ballot_sync(0xffffffffu, found >= 0);
+    const int src = fm ? __ffs(fm) - 1 : 0;
+    found = __shfl_sync(0xffffffffu, found, src);
+    frank = __shfl_sync(0xffffffffu, frank, src);
+    feq = __shfl_sync(0xffffffffu, feq, src);
+    pre = (pre << 8) | (uint32_t)(found < 0 ? 0 : found);
+    rank = frank;
+    eq = feq;
+    __syncwarp();
+  }
+  *rank_out = rank;
+  *eq_out = eq;
+  return pre;
+}
+
+// Bitonic sort of cnt (<= kCand) composites ascending, padded with ~0.
+__device__ void warp_sort(unsigned long long *a, int cnt, int lane) {
+  int m = 32;
+  while (m < cnt) m <<= 1;
+  for (int i = cnt + lane; i < m; i += 32) a[i] = ~0ull;
+  __syncwarp();
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < m; i += 32) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long x = a[i], y = a[l];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[l] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
+                                                          MoveArgs M, int64_t T_heads) {
+  __shared__ WarpArea area[kWC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kWC + warp;
+  if (g >= T_heads) return;
+  WarpArea &A = area[warp];
+  const int si = (int)(g / S.hp), hi = (int)(g % S.hp);
+  const int e = M.evict[g];
+  if (lane == 0 && M.move_counts) M.move_counts[g] = 0;
+  if (lane == 0 && M.evicted_kvs) M.evicted_kvs[g] = 0;
+  if (e <= 0) return;
+  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+  const int nb = p.nblocks[hidx];
+  const int C = p.ctx[hidx];
+  const int n = nb * 16;
+  const int32_t *tab = head_table(p, hidx);
+  const uint32_t *keys = S.keys + g * S.max_slots;
+  auto sec = [&](int pos, int32_t lg) -> uint32_t {
+    return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
+  };
+  auto lg_at = [&](int pos) -> int32_t { return p.logical[(int64_t)tab[pos >> 4] * 16 + (pos & 15)]; };
+  // collect composites of the positions whose key satisfies pred; returns the count
+  auto collect = [&](auto pred) -> int {
+    int cnt = 0;
+    for (int base = 0; base < n; base += 1024) {  // 8 uint4 per lane in flight
+      uint4 k4[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int pos0 = base + (u * 32 + lane) * 4;
+        k4[u] = pos0 < n ? *reinterpret_cast<const uint4 *>(keys + pos0) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int pos0 = base + (u * 32 + lane) * 4;
+        const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool ok = pos0 + i < n && pred(kv[i]);
+          const unsigned bm = __ballot_sync(0xffffffffu, ok);
+          if (bm) {
+            const int slot = cnt + __popc(bm & ((1u << lane) - 1u));
+            if (ok && slot < kCand) A.cand[slot] = ((unsigned long long)kv[i] << 32) | sec(pos0 + i, lg_at(pos0 + i));
+            cnt += __popc(bm);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    return cnt;
+  };
+  // ---- threshold T_h and tie cut Sx: masked iff (key, sec) <= (T, Sx) ----
+  const uint32_t Tstar = S.prefix[si];
+  const int64_t lt = S.ltc[g], le = S.lec[g];
+  const int64_t target = (int64_t)16 * e - 1;
+  uint32_t T, Sx = 0xffffffffu;
+  int32_t *hist = reinterpret_cast<int32_t *>(A.cand);
+  if (target >= lt) {
+    T = Tstar;
+    const int64_t tie_rank = target - lt, tie_cnt = le - lt;
+    if (tie_rank + 1 < tie_cnt) {
+      if (tie_cnt <= kCand) {
+        const int cnt = collect([&](uint32_t k) { return k == Tstar; });
+        warp_sort(A.cand, cnt, lane);
+        Sx = (uint32_t)(A.cand[tie_rank] & 0xffffffffu);
+      } else {
+        int64_t d0, d1;
+        Sx = warp_select(hist, n, tie_rank, [&](int pos, uint32_t &v) {
+          if (keys[pos] != Tstar) return false;
+          v = sec(pos, lg_at(pos));
+          return true;
+        }, lane, &d0, &d1);
+      }
+    }
+  } else if (lt <= kCand) {
+    const int cnt = collect([&](uint32_t k) { return k < Tstar; });
+    warp_sort(A.cand, cnt, lane);
+    const unsigned long long c = A.cand[target];
+    T = (uint32_t)(c >> 32);
+    Sx = (uint32_t)(c & 0xffffffffu);
+  } else {
+    int64_t tie_rank, tie_cnt;
+    T = warp_select(hist, n, target, [&](int pos, uint32_t &v) { v = keys[pos]; return v < Tstar; }, lane,
+                    &tie_rank, &tie_cnt);
+    if (tie_rank + 1 < tie_cnt) {
+      int64_t d0, d1;
+      Sx = warp_select(hist, n, tie_rank, [&](int pos, uint32_t &v) {
+        if (keys[pos] != T) return false;
+        v = sec(pos, lg_at(pos));
+        return true;
+      }, lane, &d0, &d1);
+    }
+  }
+  __syncwarp();
+  auto block_flags = [&](int bl, int64_t f0, uint32_t &mb, uint32_t &lb) {
+    const uint4 *kp = reinterpret_cast<const uint4 *>(keys + bl * 16);
+    const int4 *lp = reinterpret_cast<const int4 *>(p.logical + f0);
+    mb = 0;
+    lb = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 k4 = kp[q];
+      const int4 l4 = lp[q];
+      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int o = q * 4 + i;
+        const bool m = kv[i] < T || (kv[i] == T && sec(bl * 16 + o, lv[i]) <= Sx);
+        mb |= (m ? 1u : 0u) << o;
+        lb |= (lv[i] >= 0 ? 1u : 0u) << o;
+      }
+    }
+  };
+  auto occ_bits = [&](int bl) -> uint32_t {
+    const int occ_n = C - bl * 16;
+    return occ_n >= 16 ? 0xffffu : occ_n <= 0 ? 0u : ((1u << occ_n) - 1u);
+  };
+  const int rb = nb - e;
+  int32_t *mv = M.moves + M.move_off[g] * 2;
+  const int64_t cap_mv = (int64_t)16 * e;
+  int evk = 0;
+  // ---- holes ascending below the range ----
+  int nholes = 0;
+  for (int base = 0; base < rb; base += 64) {  // blocks base+lane and base+32+lane: loads of both in flight
+    uint32_t holes[2] = {0u, 0u};
+    int64_t f0[2] = {0, 0};
+    uint32_t mb[2], lb[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int bl = base + u * 32 + lane;
+      if (bl < rb) f0[u] = (int64_t)tab[bl] * 16;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int bl = base + u * 32 + lane;
+      if (bl < rb) {
+        block_flags(bl, f0[u], mb[u], lb[u]);
+        holes[u] = (mb[u] | ~lb[u]) & 0xffffu;
+        evk += __popc(mb[u] & occ_bits(bl));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int tot;
+      int k = nholes + warp_excl_scan(__popc(holes[u]), lane, tot);
+      for (uint32_t hb = holes[u]; hb; hb &= hb - 1) {
+        if (k < cap_mv) mv[2 * k + 1] = (int32_t)(f0[u] + __ffs(hb) - 1);
+        ++k;
+      }
+      nholes += tot;
+    }
+  }
+  // ---- survivors descending inside the range ----
+  int nmoves = 0;
+  for (int base = 0; base < e; base += 32) {
+    const int t = base + lane;
+    const int bl = nb - 1 - t;
+    uint32_t surv = 0;
+    int64_t f0 = 0;
+    if (t < e) {
+      f0 = (int64_t)tab[bl] * 16;
+      uint32_t mb, lb;
+      block_flags(bl, f0, mb, lb);
+      surv = ~mb & lb & 0xffffu;
+      evk += __popc(mb & occ_bits(bl));
+    }
+    int tot;
+    int k = nmoves + warp_excl_scan(__popc(surv), lane, tot);
+    for (int o = 15; o >= 0; --o) {
+      if (surv >> o & 1u) {
+        if (k < cap_mv) mv[2 * k] = (int32_t)(f0 + o);
+        ++k;
+      }
+    }
+    nmoves += tot;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) evk += __shfl_xor_sync(0xffffffffu, evk, o);
+  __syncwarp();
+  if (nmoves > nholes) {
+    if (lane == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
+    return;
+  }
+  // ---- pair metadata (holes below the range, survivors inside: disjoint) ----
+  for (int k = lane; k < nmoves; k += 32) {
+    const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
+    p.metric[dst] = p.metric[src];
+    p.logical[dst] = p.logical[src];
+    p.protected_[dst] = p.protected_[src];
+    p.fresh[dst] = p.fresh[src];
+  }
+  __syncwarp();
+  // ---- free the trailing e blocks and reset their slots ----
+  for (int t = lane; t < e; t += 32) {
+    const int32_t blk = tab[rb + t];
+    const int64_t f0 = (int64_t)blk * 16;
+    float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
+    int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      lp[q] = make_int4(-1, -1, -1, -1);
+    }
+    *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
+    p.free_flag[blk] = 1;
+    atomicAdd(&p.free_tile[blk / KVC_FREE_TILE], 1);
+    if (M.freed) M.freed[g * p.max_blocks + t] = blk;
+  }
+  // ---- logical renumbering: rank among the kept logicals ----
+  const int Cn = C < rb * 16 ? C : rb * 16;
+  const int words = (n + 31) / 32;
+  for (int w = lane; w < words; w += 32) A.bitmap[w] = 0;
+  __syncwarp();
+  const int kb = (Cn + 15) / 16;
+  for (int bl0 = lane; bl0 < kb; bl0 += 64) {
+    int4 l4s[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int bl = bl0 + 32 * u;
+      if (bl < kb) {
+        const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) l4s[u][q] = lp[q];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+    const int bl = bl0 + 32 * u;
+    if (bl >= kb) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 l4 = l4s[u][q];
+      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pos = bl * 16 + q * 4 + i;
+        if (pos >= Cn) continue;
+        const int32_t lg = lv[i];
+        if (lg < 0 || lg >= n) {
+          set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+          continue;
+        }
+        const uint32_t bit = 1u << (lg & 31);
+        if (atomicOr(&A.bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+      }
+    }
+    }
+  }
+  __syncwarp();
+  {
+    int c[8], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int w = lane * 8 + i;
+      c[i] = w < words ? __popc(A.bitmap[w]) : 0;
+      sum += c[i];
+    }
+    int tot;
+    int run = warp_excl_scan(sum, lane, tot);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int w = lane * 8 + i;
+      if (w < words) A.wpre[w] = run;
+      run += c[i];
+    }
+  }
+  __syncwarp();
+  for (int bl0 = lane; bl0 < kb; bl0 += 64) {
+    int4 l4s[2][4];
+    int4 *lps[2] = {nullptr, nullptr};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int bl = bl0 + 32 * u;
+      if (bl < kb) {
+        lps[u] = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) l4s[u][q] = lps[u][q];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+    const int bl = bl0 + 32 * u;
+    if (bl >= kb) continue;
+    int4 *lp = lps[u];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 l4 = l4s[u][q];
+      int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int pos = bl * 16 + q * 4 + i;
+        const int32_t lg = lv[i];
+        if (pos >= Cn || lg < 0 || lg >= n) continue;
+        lv[i] = A.wpre[lg >> 5] + __popc(A.bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
+      }
+      lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+    }
+    }
+  }
+  if (lane == 0) {
+    p.nblocks[hidx] = rb;
+    p.ctx[hidx] = Cn;
+    if (M.move_counts) M.move_counts[g] = nmoves;
+    if (M.evicted_kvs) M.evicted_kvs[g] = evk;
+    if (M.totals) {
+      atomicAdd((unsigned long long *)&M.totals[0], (unsigned long long)e);
+      atomicAdd((unsigned long long *)&M.totals[1], (unsigned long long)evk);
+      atomicAdd((unsigned long long *)&M.totals[2], (unsigned long long)nmoves);
+    }
+  }
+}
+
+// K/V rows of every move of the round, as one flat persistent grid: warp
+// tasks of 32 consecutive move-list entries (the lists are laid out by the
+// exclusive offsets of e_h * b); each lane finds its entry's head by binary
+// search over the offsets and keeps it if it is below that head's move count.
+// The valid moves' rows are then copied in 16-byte chunks (2-byte elements
+// for head_dim % 8 != 0), several chunks in flight per lane.  Sources are in
+// blocks freed by k_compact; nothing can reuse them before this kernel
+// completes (stream order).
+template <typename Chunk>
+__device__ __forceinline__ void copy_rows(Chunk *kc, Chunk *vc, const int64_t *src, const int64_t *dst, int nvalid,
+                                          int per_row, int lane) {
+  const int nch = 2 * per_row;  // K chunks then V chunks
+  const int total = nvalid * nch;
+  for (int i0 = 0; i0 < total; i0 += 32 * 4) {
+    Chunk val[4];
+    int64_t to[4];
+    bool isv[4], ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = i0 + u * 32 + lane;
+      ok[u] = idx < total;
+      if (ok[u]) {
+        const int m = idx / nch, c0 = idx % nch;
+        isv[u] = c0 >= per_row;
+        const int c = isv[u] ? c0 - per_row : c0;
+        const Chunk *base = isv[u] ? vc : kc;
+        val[u] = base[src[m] * per_row + c];
+        to[u] = dst[m] * per_row + c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ok[u]) (isv[u] ? vc : kc)[to[u]] = val[u];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_copy_kv(kvc_pool p, const int32_t *moves, const int64_t *move_off,
+                                                const int32_t *move_counts, int64_t T) {
+  __shared__ int64_t s_src[8][32], s_dst[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t cap = move_off[T];
+  const int64_t tasks = (cap + 31) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  const int D = p.head_dim;
+  for (int64_t task = (int64_t)blockIdx.x * 8 + warp; task < tasks; task += nwarps) {
+    const int64_t k = task * 32 + lane;
+    bool valid = false;
+    if (k < cap) {
+      int64_t lo = 0, hi = T - 1;  // last g with move_off[g] <= k
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(move_off + mid) <= k) lo = mid;
+        else hi = mid - 1;
+      }
+      valid = k - move_off[lo] < move_counts[lo];
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const int r = __popc(vm & ((1u << lane) - 1u));
+      s_src[warp][r] = moves[2 * k];
+      s_dst[warp][r] = moves[2 * k + 1];
+    }
+    __syncwarp();
+    const int nvalid = __popc(vm);
+    if (D % 8 == 0)
+      copy_rows(reinterpret_cast<uint4 *>(p.k_cache), reinterpret_cast<uint4 *>(p.v_cache), s_src[warp], s_dst[warp],
+                nvalid, D / 8, lane);
+    else
+      copy_rows(reinterpret_cast<uint16_t *>(p.k_cache), reinterpret_cast<uint16_t *>(p.v_cache), s_src[warp],
+                s_dst[warp], nvalid, D, lane);
+    __syncwarp();
+  }
+}
+
+// K/V rows of every move of the round for long heads: grid (head, part); a warp moves one
 // (K, V) row pair per step with 16-byte lanes, 4 pairs in flight per warp.
 // Sources are inside blocks freed by k_compact; nothing can reuse them before
 // this kernel completes (stream order).
-__global__ void __launch_bounds__(256) k_copy_kv(kvc_pool p, const int32_t *moves, const int64_t *move_off,
+__global__ void __launch_bounds__(256) k_copy_kv_heads(kvc_pool p, const int32_t *moves, const int64_t *move_off,
                                                 const int32_t *move_counts) {
   const int g = blockIdx.x;
   const int n = move_counts[g];
@@ -1112,16 +1895,32 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
   if (pool->block_size == 16) {
     static bool conf16 = false;
     if (!conf16) {
-      cudaFuncSetAttribute(k_compact16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_compact_smem<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_compact16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       conf16 = true;
     }
-    if (small_heads(S)) k_compact16<256><<<(int)T, 256, dyn, s>>>(*pool, a->seq_rows, S, M);
+    static const bool use_smem = getenv("KVC_K4_SMEM") != nullptr;
+    if (small_heads(S) && use_smem) {
+      const int dyn_s = (int)(8 * S.max_slots) + 8 * words + 64;
+      k_compact_smem<256><<<(int)T, 256, dyn_s, s>>>(*pool, a->seq_rows, S, M);
+    } else if (small_heads(S)) {
+      k_compact_warp<<<(unsigned)((T + kWC - 1) / kWC), kWC * 32, 0, s>>>(*pool, a->seq_rows, S, M, T);
+    }
     else k_compact16<1024><<<(int)T, 1024, dyn, s>>>(*pool, a->seq_rows, S, M);
   } else {
     k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
   }
-  if (pool->k_cache) k_copy_kv<<<dim3((unsigned)T, 8), 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts);
+  if (pool->k_cache && T > 0) {
+    static int n_sm = 0;
+    if (!n_sm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // short heads (few moves each): one flat grid; long heads: a CTA row per head
+    if (small_heads(S)) k_copy_kv<<<n_sm * 8, 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts, T);
+    else k_copy_kv_heads<<<dim3((unsigned)T, 8), 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts);
+  }
   if (a->totals) k_free_total<<<1, 1024, 0, s>>>(*pool, a->totals);
   KVC_CHECK_LAUNCH();
   return KVC_OK;
