@@ -37,6 +37,7 @@ namespace {
 constexpr int kBins = 2048;       // 11-bit digits
 constexpr int kThreads = 512;
 constexpr uint32_t kKeyInf = 0xFF800000u;  // f32_order_key(+inf)
+constexpr int kCand = 256;                 // candidate list capacity per head (short-head path)
 
 struct EvictState {
   // per head (T = n_seqs * hp)
@@ -51,6 +52,7 @@ struct EvictState {
   uint32_t *prefix;   // [n_seqs] T* digits found so far
   int64_t *E;         // [n_seqs] clamped budget (0 = inactive)
   int64_t *seq_moves; // [n_seqs] move slots of the sequence, then its base offset
+  unsigned long long *cand;  // nullable [T][2][kCand]: (key << 32 | secondary) of keys < T* / == T*
   int64_t max_slots;
   int hp;
   int32_t *status;
@@ -296,11 +298,14 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
   add_contrib<NT>(hist, (int32_t)below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
 }
 
-// (7) per head: rows with threshold < T* and <= T*.
+// (7) per head: rows with threshold < T* and <= T*.  With S.cand, also the
+// composites (key << 32 | secondary) of the keys < T* and of the ties at T*
+// (first kCand of each, any order) for k_compact_warp.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, EvictState S) {
   using Red = cub::BlockReduce<int32_t, NT>;
   __shared__ typename Red::TempStorage tmp;
+  __shared__ int32_t cnt_s[2];
   const int g = blockIdx.x;
   const int si = g / S.hp, hi = g % S.hp;
   if (S.E[si] <= 0) {
@@ -310,13 +315,68 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
   const int b = p.block_size;
   const int64_t n = (int64_t)p.nblocks[hidx] * b;
+  const int C = p.ctx[hidx];
+  const int32_t *tab = head_table(p, hidx);
   const uint32_t T = S.prefix[si];
   const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+  unsigned long long *cand = S.cand ? S.cand + (int64_t)g * 2 * kCand : nullptr;
+  if (threadIdx.x < 2) cnt_s[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   int32_t lt = 0, le = 0;
-  for (int64_t pos = threadIdx.x; pos < n; pos += NT) {
-    const uint32_t k = keys[pos];
-    lt += k < T;
-    le += k <= T;
+  if (!cand) {
+    for (int64_t pos = threadIdx.x; pos < n; pos += NT) {
+      const uint32_t k = keys[pos];
+      lt += k < T;
+      le += k <= T;
+    }
+  } else {
+    // short heads (n <= 8192): all of the head's keys in flight at once, 4
+    // per uint4; match masks per thread, then block scans place the
+    // candidates (no per-element votes)
+    constexpr int U = 8192 / (4 * NT);
+    uint4 k4[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int pos0 = (u * NT + threadIdx.x) * 4;
+      k4[u] = pos0 < n ? *reinterpret_cast<const uint4 *>(keys + pos0) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+    uint32_t mlt = 0, meq = 0;  // bit u*4+i
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int pos0 = (u * NT + threadIdx.x) * 4;
+      const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool in = pos0 + i < n;
+        mlt |= (in && kv[i] < T ? 1u : 0u) << (u * 4 + i);
+        meq |= (in && kv[i] == T ? 1u : 0u) << (u * 4 + i);
+      }
+    }
+    using Scan = cub::BlockScan<int32_t, NT>;
+    __shared__ typename Scan::TempStorage stmp;
+    __shared__ int32_t tot_s[2];
+    const uint32_t masks[2] = {mlt, meq};
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      int32_t excl, tot;
+      Scan(stmp).ExclusiveSum(__popc(masks[l]), excl, tot);
+      if (threadIdx.x == 0) tot_s[l] = tot;
+      __syncthreads();
+      if (tot_s[l] <= kCand) {
+        for (uint32_t mb = masks[l]; mb; mb &= mb - 1) {
+          const int bit = __ffs(mb) - 1;
+          const int u = bit >> 2, i = bit & 3;
+          const int pos = (u * NT + threadIdx.x) * 4 + i;
+          const uint32_t kk = keys[pos];  // (re-read: indexing k4 here would put it in local memory)
+          const int32_t lg = p.logical[(int64_t)tab[pos >> 4] * 16 + (pos & 15)];
+          const uint32_t sc = pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
+          cand[l * kCand + excl++] = ((unsigned long long)kk << 32) | sc;
+        }
+      }
+    }
+    lt = __popc(mlt);
+    le = lt + __popc(meq);
   }
   lt = Red(tmp).Sum(lt);
   __syncthreads();
@@ -335,17 +395,18 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
 __global__ void __launch_bounds__(1024) k_select(EvictState S, int bsz, int32_t *evict, int64_t *move_off,
                                                 int32_t *status) {
   using Scan = cub::BlockScan<int64_t, 1024>;
+  using Red = cub::BlockReduce<int64_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
+  __shared__ typename Red::TempStorage rtmp;
   __shared__ int64_t less_s;
   const int hp = S.hp;
   const int si = blockIdx.x;
   const int64_t E = S.E[si];
   // total rows strictly below T*
-  if (threadIdx.x == 0) less_s = 0;
-  __syncthreads();
   int64_t less = 0;
   for (int h = threadIdx.x; h < hp; h += 1024) less += E > 0 ? S.lo[(int64_t)si * hp + h] : 0;
-  atomicAdd((unsigned long long *)&less_s, (unsigned long long)less);
+  less = Red(rtmp).Sum(less);
+  if (threadIdx.x == 0) less_s = less;
   __syncthreads();
   const int64_t need = E - less_s;  // tie rows to take at T*, in head order
   int64_t tcarry = 0, ocarry = 0;
@@ -953,298 +1014,6 @@ __global__ void __launch_bounds__(NT) k_compact16(kvc_pool p, const int32_t *row
 }
 
 // ---------------------------------------------------------------------------
-// k_compact_smem: k_compact16 for heads of at most 8192 slots (the
-// decode-time batch).  The head's keys and logicals are staged in shared
-// memory once; both radix selects (8-bit digits, 4 levels) and the logical
-// renumbering run there, so the CTA's dependent global round trips are the
-// stage-in, the move/free metadata writes and the logical write-back.
-// Same pairing and renumbering as k_compact16 (compression.py:234-309).
-// ---------------------------------------------------------------------------
-
-// rank-th smallest (0-based) of getv over [0, n) (valid entries only); also
-// its rank among equal values and their count.  hist: 256 ints of smem.
-template <int NT, typename GetV>
-__device__ uint32_t smem_select(int32_t *hist, int n, int64_t rank, GetV getv, int64_t *rank_out, int64_t *eq_out) {
-  using Scan = cub::BlockScan<int32_t, NT>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ uint32_t pre_s;
-  __shared__ int64_t rank_s, eq_s;
-  static_assert(NT >= 256, "one bin per thread");
-  uint32_t pre = 0;
-  int64_t eq = 0;
-  for (int lv = 0; lv < 4; ++lv) {
-    const int shift = 24 - 8 * lv;
-    if (threadIdx.x < 256) hist[threadIdx.x] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += NT) {
-      uint32_t v;
-      if (getv(i, v) && (lv == 0 || (v >> (shift + 8)) == pre)) atomicAdd(&hist[(v >> shift) & 255], 1);
-    }
-    __syncthreads();
-    const int32_t h = threadIdx.x < 256 ? hist[threadIdx.x] : 0;
-    int32_t excl;
-    Scan(tmp).ExclusiveSum(h, excl);
-    if (threadIdx.x < 256 && excl <= rank && rank < excl + h) {
-      pre_s = (pre << 8) | threadIdx.x;
-      rank_s = rank - excl;
-      eq_s = h;
-    }
-    __syncthreads();
-    pre = pre_s;
-    rank = rank_s;
-    eq = eq_s;
-  }
-  *rank_out = rank;
-  *eq_out = eq;
-  return pre;
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT) k_compact_smem(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
-  extern __shared__ __align__(16) uint32_t dyn[];
-  __shared__ int32_t hist[256];
-  __shared__ int32_t cnt_s[4];
-  using Scan = cub::BlockScan<int32_t, NT>;
-  __shared__ typename Scan::TempStorage stmp;
-  const int g = blockIdx.x;
-  const int si = g / S.hp, hi = g % S.hp;
-  const int e = M.evict[g];
-  if (threadIdx.x == 0 && M.move_counts) M.move_counts[g] = 0;
-  if (threadIdx.x == 0 && M.evicted_kvs) M.evicted_kvs[g] = 0;
-  if (e <= 0) return;
-  const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
-  const int nb = p.nblocks[hidx];
-  const int C = p.ctx[hidx];
-  const int n = nb * 16;
-  const int32_t *tab = head_table(p, hidx);
-  const int ms = (int)S.max_slots;
-  uint32_t *keys = dyn;                                     // [ms]
-  int32_t *lgs = reinterpret_cast<int32_t *>(dyn + ms);     // [ms] logical by position
-  uint32_t *bitmap = dyn + 2 * ms;                          // [ms/32]
-  int32_t *wpre = reinterpret_cast<int32_t *>(bitmap + (ms + 31) / 32);
-  // ---- stage keys and logicals by position ----
-  const uint32_t *gk = S.keys + (int64_t)g * S.max_slots;
-  for (int bl = threadIdx.x; bl < nb; bl += NT) {
-    const uint4 *kp = reinterpret_cast<const uint4 *>(gk + bl * 16);
-    const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
-    uint4 *ks = reinterpret_cast<uint4 *>(keys + bl * 16);
-    int4 *ls = reinterpret_cast<int4 *>(lgs + bl * 16);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      ks[q] = kp[q];
-      ls[q] = lp[q];
-    }
-  }
-  __syncthreads();
-  // ---- threshold T_h = (16 e)-th smallest key; shortcut when it is T* ----
-  const uint32_t Tstar = S.prefix[si];
-  const int64_t lt = S.ltc[g], le = S.lec[g];
-  const int64_t target = (int64_t)16 * e - 1;
-  uint32_t T;
-  int64_t tie_rank, tie_cnt;
-  if (target >= lt) {
-    T = Tstar;
-    tie_rank = target - lt;
-    tie_cnt = le - lt;
-  } else {
-    T = smem_select<NT>(hist, n, target, [&](int i, uint32_t &v) { v = keys[i]; return v < Tstar; }, &tie_rank,
-                        &tie_cnt);
-  }
-  // ---- tie cut: ties at T ordered by (occupied, logical, position) ----
-  auto sec = [&](int pos, int32_t lg) -> uint32_t {
-    return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
-  };
-  uint32_t Sx = 0xffffffffu;
-  if (tie_rank + 1 < tie_cnt) {
-    int64_t d0, d1;
-    Sx = smem_select<NT>(hist, n, tie_rank, [&](int i, uint32_t &v) {
-      if (keys[i] != T) return false;
-      v = sec(i, lgs[i]);
-      return true;
-    }, &d0, &d1);
-  }
-  auto block_flags = [&](int bl, uint32_t &mb, uint32_t &lb) {
-    mb = 0;
-    lb = 0;
-#pragma unroll
-    for (int o = 0; o < 16; ++o) {
-      const int pos = bl * 16 + o;
-      const uint32_t k = keys[pos];
-      const int32_t lg = lgs[pos];
-      const bool m = k < T || (k == T && (Sx == 0xffffffffu || sec(pos, lg) <= Sx));
-      mb |= (m ? 1u : 0u) << o;
-      lb |= (lg >= 0 ? 1u : 0u) << o;
-    }
-  };
-  auto occ_bits = [&](int bl) -> uint32_t {
-    const int occ_n = C - bl * 16;
-    return occ_n >= 16 ? 0xffffu : occ_n <= 0 ? 0u : ((1u << occ_n) - 1u);
-  };
-  // ---- MoveCache pairing: holes ascending below the range, survivors descending in it ----
-  const int rb = nb - e;
-  int32_t *mv = M.moves + M.move_off[g] * 2;
-  const int64_t cap_mv = (int64_t)16 * e;
-  // hole k's position is parked in keys[k]: k < #holes <= 16 rb, and the
-  // pass has finished reading keys below 16 (base + NT) when it writes them;
-  // the survivor pass reads only keys of the range (>= 16 rb)
-  int32_t *hole_pos = reinterpret_cast<int32_t *>(keys);
-  if (threadIdx.x == 0) { cnt_s[0] = 0; cnt_s[1] = 0; cnt_s[2] = 0; }
-  __syncthreads();
-  int32_t evk = 0;
-  {
-    int32_t carry = 0;
-    for (int base = 0; base < rb; base += NT) {
-      const int bl = base + threadIdx.x;
-      uint32_t holes = 0;
-      if (bl < rb) {
-        uint32_t mb, lb;
-        block_flags(bl, mb, lb);
-        holes = (mb | ~lb) & 0xffffu;
-        evk += __popc(mb & occ_bits(bl));
-      }
-      int32_t excl, tot;
-      Scan(stmp).ExclusiveSum(__popc(holes), excl, tot);
-      int64_t k = carry + excl;
-      for (uint32_t hb = holes; hb; hb &= hb - 1) {
-        const int o = __ffs(hb) - 1;
-        if (k < cap_mv) {
-          mv[2 * k + 1] = tab[bl] * 16 + o;
-          hole_pos[k] = bl * 16 + o;
-        }
-        ++k;
-      }
-      carry += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) cnt_s[0] = carry;
-  }
-  __syncthreads();
-  int32_t nmoves;
-  {
-    int32_t carry = 0;
-    for (int base = 0; base < e; base += NT) {
-      const int t = base + threadIdx.x;
-      const int bl = nb - 1 - t;
-      uint32_t surv = 0;
-      if (t < e) {
-        uint32_t mb, lb;
-        block_flags(bl, mb, lb);
-        surv = ~mb & lb & 0xffffu;
-        evk += __popc(mb & occ_bits(bl));
-      }
-      int32_t excl, tot;
-      Scan(stmp).ExclusiveSum(__popc(surv), excl, tot);
-      int64_t k = carry + excl;
-      const int64_t f0 = t < e ? (int64_t)tab[bl] * 16 : 0;
-      for (int o = 15; o >= 0; --o) {
-        if (surv >> o & 1u) {
-          if (k < cnt_s[0]) {
-            mv[2 * k] = (int32_t)(f0 + o);
-            hole_pos[k] |= (bl * 16 + o) << 16;  // pair k: hole position | survivor position << 16
-          }
-          ++k;
-        }
-      }
-      carry += tot;
-      __syncthreads();
-    }
-    nmoves = carry;
-  }
-  atomicAdd(&cnt_s[2], evk);
-  __syncthreads();
-  if (nmoves > cnt_s[0]) {
-    if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
-    return;
-  }
-  // metadata of every pair, one pair per thread (holes lie below the range,
-  // survivors inside it: no pair reads a slot another pair writes)
-  for (int k = threadIdx.x; k < nmoves; k += NT) {
-    const int hp_ = hole_pos[k] & 0xffff, sp_ = hole_pos[k] >> 16;
-    const int64_t dst = (int64_t)tab[hp_ >> 4] * 16 + (hp_ & 15);
-    const int64_t src = (int64_t)tab[sp_ >> 4] * 16 + (sp_ & 15);
-    p.metric[dst] = p.metric[src];
-    p.protected_[dst] = p.protected_[src];
-    p.fresh[dst] = p.fresh[src];
-    lgs[hp_] = lgs[sp_];
-  }
-  __syncthreads();
-  // ---- free the trailing e blocks and reset their slots ----
-  for (int t = threadIdx.x; t < e; t += NT) {
-    const int j = rb + t;
-    const int32_t blk = tab[j];
-    const int64_t f0 = (int64_t)blk * 16;
-    float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
-    int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      lp[q] = make_int4(-1, -1, -1, -1);
-    }
-    *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
-    p.free_flag[blk] = 1;
-    atomicAdd(&p.free_tile[blk / KVC_FREE_TILE], 1);
-    if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
-  }
-  const int keep = rb;
-  const int Cn = C < keep * 16 ? C : keep * 16;
-  // ---- logical renumbering: rank among the kept logicals ----
-  const int words = (n + 31) / 32;
-  for (int w = threadIdx.x; w < words; w += NT) bitmap[w] = 0;
-  __syncthreads();
-  for (int pos = threadIdx.x; pos < Cn; pos += NT) {
-    const int32_t lg = lgs[pos];
-    if (lg < 0 || lg >= n) {
-      set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
-      continue;
-    }
-    const uint32_t bit = 1u << (lg & 31);
-    if (atomicOr(&bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
-  }
-  __syncthreads();
-  {
-    int32_t carry = 0;
-    for (int base = 0; base < words; base += NT) {
-      const int w = base + threadIdx.x;
-      const int32_t c = w < words ? __popc(bitmap[w]) : 0;
-      int32_t excl, tot;
-      Scan(stmp).ExclusiveSum(c, excl, tot);
-      if (w < words) wpre[w] = carry + excl;
-      carry += tot;
-      __syncthreads();
-    }
-  }
-  __syncthreads();
-  const int kb = (Cn + 15) / 16;
-  for (int bl = threadIdx.x; bl < kb; bl += NT) {
-    int4 *lp = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int32_t lv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int pos = bl * 16 + q * 4 + i;
-        const int32_t lg = lgs[pos];
-        lv[i] = (pos >= Cn || lg < 0 || lg >= n) ? lg
-                : (int32_t)wpre[lg >> 5] + __popc(bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
-      }
-      lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
-    }
-  }
-  if (threadIdx.x == 0) {
-    p.nblocks[hidx] = keep;
-    p.ctx[hidx] = Cn;
-    if (M.move_counts) M.move_counts[g] = nmoves;
-    if (M.evicted_kvs) M.evicted_kvs[g] = cnt_s[2];
-    if (M.totals) {
-      atomicAdd((unsigned long long *)&M.totals[0], (unsigned long long)e);
-      atomicAdd((unsigned long long *)&M.totals[1], (unsigned long long)cnt_s[2]);
-      atomicAdd((unsigned long long *)&M.totals[2], (unsigned long long)nmoves);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // k_compact_warp: one warp per head for heads of at most 8192 slots (the
 // decode-time batch: thousands of short heads, a few evicted blocks each).
 // No CTA barriers; 8 heads per CTA, 4 KB of shared memory per warp.
@@ -1255,7 +1024,6 @@ __global__ void __launch_bounds__(NT) k_compact_smem(kvc_pool p, const int32_t *
 //    one 16-slot block per lane with warp scans.
 // ---------------------------------------------------------------------------
 constexpr int kWC = 8;      // warps (heads) per CTA
-constexpr int kCand = 256;  // candidate capacity per warp
 
 struct WarpArea {
   unsigned long long cand[kCand];  // composites (key << 32 | secondary); or a 256-bin histogram
@@ -1369,34 +1137,11 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
     return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
   };
   auto lg_at = [&](int pos) -> int32_t { return p.logical[(int64_t)tab[pos >> 4] * 16 + (pos & 15)]; };
-  // collect composites of the positions whose key satisfies pred; returns the count
-  auto collect = [&](auto pred) -> int {
-    int cnt = 0;
-    for (int base = 0; base < n; base += 1024) {  // 8 uint4 per lane in flight
-      uint4 k4[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int pos0 = base + (u * 32 + lane) * 4;
-        k4[u] = pos0 < n ? *reinterpret_cast<const uint4 *>(keys + pos0) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int pos0 = base + (u * 32 + lane) * 4;
-        const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const bool ok = pos0 + i < n && pred(kv[i]);
-          const unsigned bm = __ballot_sync(0xffffffffu, ok);
-          if (bm) {
-            const int slot = cnt + __popc(bm & ((1u << lane) - 1u));
-            if (ok && slot < kCand) A.cand[slot] = ((unsigned long long)kv[i] << 32) | sec(pos0 + i, lg_at(pos0 + i));
-            cnt += __popc(bm);
-          }
-        }
-      }
-    }
+  // candidate list l (0: keys < T*, 1: ties at T*) written by k_bounds -> smem
+  auto load_cand = [&](int l, int cnt) {
+    const unsigned long long *src = S.cand + g * 2 * kCand + l * kCand;
+    for (int i = lane; i < cnt; i += 32) A.cand[i] = src[i];
     __syncwarp();
-    return cnt;
   };
   // ---- threshold T_h and tie cut Sx: masked iff (key, sec) <= (T, Sx) ----
   const uint32_t Tstar = S.prefix[si];
@@ -1409,7 +1154,8 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
     const int64_t tie_rank = target - lt, tie_cnt = le - lt;
     if (tie_rank + 1 < tie_cnt) {
       if (tie_cnt <= kCand) {
-        const int cnt = collect([&](uint32_t k) { return k == Tstar; });
+        const int cnt = (int)tie_cnt;
+        load_cand(1, cnt);
         warp_sort(A.cand, cnt, lane);
         Sx = (uint32_t)(A.cand[tie_rank] & 0xffffffffu);
       } else {
@@ -1422,7 +1168,8 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
       }
     }
   } else if (lt <= kCand) {
-    const int cnt = collect([&](uint32_t k) { return k < Tstar; });
+    const int cnt = (int)lt;
+    load_cand(0, cnt);
     warp_sort(A.cand, cnt, lane);
     const unsigned long long c = A.cand[target];
     T = (uint32_t)(c >> 32);
@@ -1441,6 +1188,13 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
     }
   }
   __syncwarp();
+  // kept-logical bitmap built while the passes read the logicals: the kept
+  // set is the logicals of unmasked live slots whenever every hole is filled
+  // (the normal case); otherwise it is rebuilt after the moves below
+  const int words = (n + 31) / 32;
+  for (int w = lane; w < words; w += 32) A.bitmap[w] = 0;
+  __syncwarp();
+  bool bad = false;
   auto block_flags = [&](int bl, int64_t f0, uint32_t &mb, uint32_t &lb) {
     const uint4 *kp = reinterpret_cast<const uint4 *>(keys + bl * 16);
     const int4 *lp = reinterpret_cast<const int4 *>(p.logical + f0);
@@ -1458,6 +1212,14 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
         const bool m = kv[i] < T || (kv[i] == T && sec(bl * 16 + o, lv[i]) <= Sx);
         mb |= (m ? 1u : 0u) << o;
         lb |= (lv[i] >= 0 ? 1u : 0u) << o;
+        if (!m && lv[i] >= 0) {
+          if (lv[i] >= n) {
+            bad = true;
+          } else {
+            const uint32_t bit = 1u << (lv[i] & 31);
+            if (atomicOr(&A.bitmap[lv[i] >> 5], bit) & bit) bad = true;
+          }
+        }
       }
     }
   };
@@ -1559,10 +1321,13 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
   }
   // ---- logical renumbering: rank among the kept logicals ----
   const int Cn = C < rb * 16 ? C : rb * 16;
-  const int words = (n + 31) / 32;
+  const int kb = (Cn + 15) / 16;
+  const bool fast = nholes == nmoves;
+  if (fast) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, -1);
+  } else {
   for (int w = lane; w < words; w += 32) A.bitmap[w] = 0;
   __syncwarp();
-  const int kb = (Cn + 15) / 16;
   for (int bl0 = lane; bl0 < kb; bl0 += 64) {
     int4 l4s[2][4];
 #pragma unroll
@@ -1596,6 +1361,7 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
       }
     }
     }
+  }
   }
   __syncwarp();
   {
@@ -1641,7 +1407,11 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
       for (int i = 0; i < 4; ++i) {
         const int pos = bl * 16 + q * 4 + i;
         const int32_t lg = lv[i];
-        if (pos >= Cn || lg < 0 || lg >= n) continue;
+        if (pos >= Cn) continue;
+        if (lg < 0 || lg >= n) {
+          if (fast) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+          continue;
+        }
         lv[i] = A.wpre[lg >> 5] + __popc(A.bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
       }
       lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
@@ -1817,6 +1587,11 @@ __global__ void k_free_total(kvc_pool p, int64_t *totals) {
   if (threadIdx.x == 0) totals[3] = s;
 }
 
+// Threads per head for the histogram passes and the compaction: heads of at
+// most 8192 slots (the decode-time batch) use small CTAs / one warp so more
+// heads are resident at once; long prefill heads use wide CTAs.
+static bool small_heads(const EvictState &S) { return S.max_slots <= 8192; }
+
 int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, EvictState &S) {
   S.hp = pool->num_layers * pool->num_kv_heads;
   S.max_slots = (a->max_slots_per_head + 3) & ~int64_t(3);  // uint4 key rows
@@ -1832,7 +1607,10 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
   S.seq_moves = sc.take<int64_t>(a->n_seqs);
-  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.prefix || !S.E || !S.seq_moves)
+  // candidate lists for the warp-per-head compaction of short heads
+  S.cand = small_heads(S) && pool->block_size == 16 ? sc.take<unsigned long long>(T * 2 * kCand) : nullptr;
+  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.prefix || !S.E || !S.seq_moves ||
+      (small_heads(S) && pool->block_size == 16 && !S.cand))
     return KVC_ERR_INVALID;
   return KVC_OK;
 }
@@ -1844,11 +1622,6 @@ int validate(const kvc_pool *pool, const kvc_evict_args *a) {
   if (a->max_slots_per_head < 1) return KVC_ERR_INVALID;
   return KVC_OK;
 }
-
-// Threads per head for the histogram passes and the compaction: heads of at
-// most 8192 slots (the decode-time batch) use small CTAs so more heads are
-// resident at once; long prefill heads use wide ones.
-static bool small_heads(const EvictState &S) { return S.max_slots <= 8192; }
 
 int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
   const int64_t T = (int64_t)a->n_seqs * S.hp;
@@ -1895,15 +1668,10 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
   if (pool->block_size == 16) {
     static bool conf16 = false;
     if (!conf16) {
-      cudaFuncSetAttribute(k_compact_smem<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_compact16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       conf16 = true;
     }
-    static const bool use_smem = getenv("KVC_K4_SMEM") != nullptr;
-    if (small_heads(S) && use_smem) {
-      const int dyn_s = (int)(8 * S.max_slots) + 8 * words + 64;
-      k_compact_smem<256><<<(int)T, 256, dyn_s, s>>>(*pool, a->seq_rows, S, M);
-    } else if (small_heads(S)) {
+    if (small_heads(S)) {
       k_compact_warp<<<(unsigned)((T + kWC - 1) / kWC), kWC * 32, 0, s>>>(*pool, a->seq_rows, S, M, T);
     }
     else k_compact16<1024><<<(int)T, 1024, dyn, s>>>(*pool, a->seq_rows, S, M);
