@@ -62,6 +62,21 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d_hint(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -348,74 +363,177 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Fused single-pass K2 (cooperative launch): every CTA owns <= kMaxT tiles of
-// one head and keeps their score tiles resident in TMEM, so K is read from
-// HBM exactly once.  Per-head grid barriers separate (1) the softmax
-// statistics, (2) the metric of the resident tiles and (3) pooling, which
-// needs its neighbours' raw metrics.
+// Persistent K2 over every layer of a prompt (cooperative launch, one CTA per
+// SM).  CTA c owns the K tiles [t_lo, t_hi) of head h = c / cph in every
+// layer, so each layer's K is read from HBM exactly once.  Score tiles live
+// in a TMEM slot ring (S = 512 / N slots of 128 keys x N columns) that runs
+// across layers: while the epilogue warps finish layer l
+//     A  online (max, sum exp2) per column over the CTA's resident tiles
+//        -> one partial per column               -> head barrier 1
+//     B  head statistics; raw[j] = sum_col f(exp2(s - M) / Z), releasing
+//        each TMEM slot after its last read      -> head barrier 2
+//     C  centred max-pool of raw (halo from the neighbours) + per-slot
+//        install through the block table (metrics.py:57-65, 160-175)
+// the TMA warp already streams layer l+1 into the shared-memory ring and the
+// MMA warp into the slots that B frees.  Epilogue group g (4 warps, one per
+// TMEM lane quadrant) owns the tiles i with i % kGroups == g in A and B.
+// Head barriers are monotonic per-head counters (zeroed before launch).
 // ---------------------------------------------------------------------------
 
-struct FusedParams {
-  WinParams w;
-  int cph;            // CTAs per head
-  int tiles_per_cta;  // <= kMaxT
-  int *bar_cnt;       // [2][H] arrival counters (zeroed before launch)
+struct PersistParams {
+  int L, Lp, H, RW, wq, start, nl, n_q;
+  int tiles_per_head, cph;
+  float scale;      // log2(e) / sqrt(d)
+  int agg;          // 1 L1, 2 L2
+  float2 *partial;  // [H][cph][N] (m, z) per CTA and column
+  float *raw;       // [2][H][Lp] (Lp = L rounded up to 4) unpooled metric of layers l (l & 1) and l - 1
+  int *bar_cnt;     // [H] arrivals (monotonic over the launch)
   kvc_pool p;
-  int row, layer, pool, protect;
-  float *out;
+  int row, layer0, pool, protect;
+  float *out;       // [nl][H][L] pooled metrics (optional)
+  int64_t out_layer_stride;
+  unsigned long long *trace;  // debug (KVC_K2_TRACE): [grid][nl][8] globaltimer stamps
+  int dbg;                    // debug (KVC_K2_DBG): bit0 treat every tile as unmasked
 };
 
-__device__ __forceinline__ void head_barrier(int *cnt, int target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(cnt, 1);
-    while (atomicAdd(cnt, 0) < target) __nanosleep(64);
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
-template <int D>
-constexpr int fused_stages() { return D >= 256 ? 2 : D >= 128 ? 5 : 10; }
+constexpr int kPEW = 8;                // epilogue warps
+constexpr int kPGroups = kPEW / 4;     // tile groups (4 warps cover the 4 TMEM lane quadrants)
+constexpr int kPThreads = 64 + 32 * kPEW;
 
-// tcgen05 kernels run one CTA per SM here (EIATTR_RESERVED_SMEM_USED), so a
-// CTA owns the whole 512-column TMEM: 16 resident 128x32 score tiles.
-constexpr int kFusedEW = 16;  // epilogue warps: 4 per TMEM lane quadrant
+template <int D>
+constexpr int persist_stages() { return D >= 128 ? 5 : 10; }
+
+template <int N>
+__host__ __device__ constexpr int persist_rs_len(int pool) { return ((512 / N) * kTileKeys + pool + 8 + 3) & ~3; }
 
 template <int N, int D>
-__global__ void __launch_bounds__(64 + 32 * kFusedEW, 1)
-    k_window_fused(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
-                   const __grid_constant__ CUtensorMap tmK16, const FusedParams F) {
-  constexpr int kEW = kFusedEW, kGroups = kEW / 4, kNC = N / kGroups;
-  constexpr int kStages = fused_stages<D>();
+constexpr int persist_smem(int pool) {
+  return persist_stages<D>() * kTileKeys * D * 2   // K ring
+         + 2 * N * D * 2                           // Q window, double-buffered over layers
+         + persist_rs_len<N>(pool) * 4              // pooling stage (own range + halo)
+         + kPEW * N * 8                            // per-warp statistics
+         + 2 * N * 4 + N * 4                       // M, 1/Z, column limits
+         + 512 + 1024;                             // barriers, TMEM slot, alignment
+}
+
+constexpr float kNegBig = -1e30f;
+constexpr int kMaxHalf = 7;  // pool widths up to 15 take the register path in phase C  // running-max sentinel: finite, so no inf - inf
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One element of the online (max, sum exp2) with lazy rescaling, branch-free:
+// one MUFU per element; s = -inf (masked) leaves (m, z) unchanged.
+__device__ __forceinline__ void lse_step(float &m, float &z, float s) {
+  const bool up = s > m;
+  const float e = ex2_approx(up ? m - s : s - m);
+  z = up ? fmaf(z, e, 1.f) : z + e;
+  m = up ? s : m;
+}
+
+// Bit c: column h*32 + c (query head (h*32+c) / wq, window row start +
+// (h*32+c) % wq) sees key j causally; padding columns (>= RW) never do.
+__device__ __forceinline__ uint32_t window_mask(const PersistParams &P, int j, int h) {
+  uint32_t vm = 0;
+  if (j < P.L) {
+    const int dj = j - P.start;
+    int rr = (h * 32) % P.wq;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      if (h * 32 + c < P.RW && rr >= dj) vm |= 1u << c;
+      rr = rr + 1 == P.wq ? 0 : rr + 1;
+    }
+  }
+  return vm;
+}
+
+// (m, z) <- log-sum-exp merge of (m, z) and (m2, z2) in base 2.
+__device__ __forceinline__ void lse2_merge(float &m, float &z, float m2, float z2) {
+  const float mn = fmaxf(m, m2);
+  const float a = m == -INFINITY ? 0.f : z * ex2_approx(m - mn);
+  const float b = m2 == -INFINITY ? 0.f : z2 * ex2_approx(m2 - mn);
+  m = mn;
+  z = a + b;
+}
+
+// Warp reduce-scatter of 32 per-lane (m, z) columns: afterwards lane l holds
+// the merge over all 32 lanes of column l in m[0], z[0].
+__device__ __forceinline__ void warp_lse_scatter32(float *m, float *z, int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int c = 0; c < o; ++c) {
+      const float sm = up ? m[c] : m[c + o], sz = up ? z[c] : z[c + o];
+      const float km = up ? m[c + o] : m[c], kz = up ? z[c + o] : z[c];
+      const float rm = __shfl_xor_sync(0xffffffffu, sm, o);
+      const float rz = __shfl_xor_sync(0xffffffffu, sz, o);
+      float mm = km, zz = kz;
+      lse2_merge(mm, zz, rm, rz);
+      m[c] = mm;
+      z[c] = zz;
+    }
+  }
+}
+
+// Epilogue-only head barrier: named barrier over the epilogue warps, one
+// thread publishes the CTA's arrival and waits for `target` arrivals.
+__device__ __forceinline__ void epi_head_barrier(int *cnt, int target, bool leader) {
+  named_sync(1, 32 * kPEW);
+  if (leader) {
+    __threadfence();
+    atomicAdd(cnt, 1);
+    while (ld_acquire_gpu(cnt) < target) __nanosleep(32);
+    __threadfence();
+  }
+  named_sync(1, 32 * kPEW);
+}
+
+template <int N, int D>
+__global__ void __launch_bounds__(kPThreads, 1)
+    k_window_persist(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
+                     const PersistParams P) {
+  constexpr int kS = 512 / N;  // TMEM slots
+  constexpr int kStages = persist_stages<D>();
   constexpr int kAtoms = D / 64;
   constexpr int kTileBytes = kTileKeys * D * 2;
   constexpr int kQBytes = N * D * 2;
-  constexpr int kMaxT = 512 / N;  // resident score tiles (all 512 TMEM columns)
   constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
-  const WinParams &P = F.w;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *ktiles = smem;
-  uint8_t *qbuf = smem + kStages * kTileBytes;
-  int *lim_s = reinterpret_cast<int *>(qbuf + kQBytes);
+  uint8_t *qbuf = smem + kStages * kTileBytes;                      // [2][kQBytes]
+  float *rs = reinterpret_cast<float *>(qbuf + 2 * kQBytes);        // pooling stage
+  float2 *wred = reinterpret_cast<float2 *>(rs + persist_rs_len<N>(P.pool));  // [kPEW][N]
+  float *stat_s = reinterpret_cast<float *>(wred + kPEW * N);       // M[N], 1/Z[N]
+  int *lim_s = reinterpret_cast<int *>(stat_s + 2 * N);             // [N]
   uint64_t *bars = reinterpret_cast<uint64_t *>(lim_s + N);
-  uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *qfull = tfull + kMaxT;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qfull + 1);
-  float *stat_s = reinterpret_cast<float *>(tmem_slot + 4);  // M[N], invZ[N]
-  float *halfsum = stat_s + 2 * N;  // [kGroups-1][kMaxT][128] contributions of column groups >= 1
+  uint64_t *full = bars, *empty = bars + kStages, *tfull = empty + kStages, *tempty = tfull + kS;
+  uint64_t *qfull = tempty + kS, *qempty = qfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int head = blockIdx.x / F.cph, cidx = blockIdx.x % F.cph;
-  const int t_lo = cidx * F.tiles_per_cta;
-  const int t_hi = min(P.tiles_per_head, t_lo + F.tiles_per_cta);
-  const int ntiles = max(0, t_hi - t_lo);
+  const int head = blockIdx.x / P.cph, cidx = blockIdx.x % P.cph;
+  // the first (tiles % cph) CTAs take one extra tile; the last CTA, which
+  // holds the masked observation-window tile, never does
+  const int q_t = P.tiles_per_head / P.cph, rem_t = P.tiles_per_head % P.cph;
+  const int t_lo = cidx * q_t + min(cidx, rem_t);
+  const int t_hi = t_lo + q_t + (cidx < rem_t ? 1 : 0);
+  const int ntiles = t_hi - t_lo;  // >= 1, <= kS (checked on the host)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < kMaxT; ++a) mbar_init(&tfull[a], 1);
-    mbar_init(qfull, 1);
+    for (int a = 0; a < kS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&qfull[b], 1); mbar_init(&qempty[b], 1); }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) { prefetch_tmap(&tmK); prefetch_tmap(&tmQ); }
@@ -430,187 +548,276 @@ __global__ void __launch_bounds__(64 + 32 * kFusedEW, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int quad = warp & 3;
-  const int half = (warp - 2) / 4;
-  const int c0 = half * kNC;
-  const int et = threadIdx.x - 64;
-  const int key_local = quad * 32 + lane;
-
-  // ================= phase 1: stream K once, scores -> TMEM, statistics =====
   if (warp == 0) {
-    if (lane == 0 && ntiles > 0) {
-      mbar_expect_tx(qfull, kQBytes);
-      for (int a = 0; a < kAtoms; ++a) tma_load_2d(qbuf + a * N * 128, &tmQ, a * 64, head * P.RW, qfull);
-      for (int i = 0; i < ntiles; ++i) {
-        const int s = i % kStages;
-        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        mbar_expect_tx(&full[s], kTileBytes);
-        const int row0 = head * P.L + (t_lo + i) * kTileKeys;
-        if (P.dbg & 4) {
-          // 16-row boxes (many small ops in flight) into the same [atom][row] layout
-          for (int rg = 0; rg < kTileKeys / 16; ++rg)
-            for (int a = 0; a < kAtoms; ++a)
-              tma_load_2d(ktiles + s * kTileBytes + a * kTileKeys * 128 + rg * 16 * 128, &tmK16, a * 64,
-                          row0 + rg * 16, &full[s]);
-        } else {
-          tma_load_3d(ktiles + s * kTileBytes, &tmK, 0, row0, 0, &full[s]);
+    // ---------------- TMA producer: Q window per layer, K tiles ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int l = 0; l < P.nl; ++l) {
+        const int qb = l & 1;
+        if (l >= 2) mbar_wait(&qempty[qb], ((l >> 1) - 1) & 1);
+        mbar_expect_tx(&qfull[qb], kQBytes);
+        for (int a = 0; a < kAtoms; ++a)
+          tma_load_2d(qbuf + qb * kQBytes + a * N * 128, &tmQ, a * 64, (l * P.n_q) * P.wq + head * P.RW, &qfull[qb]);
+        for (int i = 0; i < ntiles; ++i) {
+          const uint32_t g = (uint32_t)(l * ntiles + i);
+          const int s = g % kStages;
+          if (g >= (uint32_t)kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
+          mbar_expect_tx(&full[s], kTileBytes);
+          const int row0 = (l * P.H + head) * P.L + (t_lo + i) * kTileKeys;
+          tma_load_3d_hint(ktiles + s * kTileBytes, &tmK, 0, row0, 0, &full[s], pol);
+          if (P.trace && i == 0) P.trace[((int64_t)blockIdx.x * P.nl + l) * 8 + 6] = gtimer();
         }
       }
     }
   } else if (warp == 1) {
-    if (ntiles > 0) {
-      mbar_wait(qfull, 0);
+    // ---------------- MMA issuer: S^T[key, col] = K . Q_w^T into TMEM slots ----------------
+    for (int l = 0; l < P.nl; ++l) {
+      const int qb = l & 1;
+      mbar_wait(&qfull[qb], (l >> 1) & 1);
       for (int i = 0; i < ntiles; ++i) {
-        const int s = i % kStages;
-        mbar_wait(&full[s], (i / kStages) & 1);
+        const uint32_t g = (uint32_t)(l * ntiles + i);
+        const int s = g % kStages, slot = g % kS;
+        mbar_wait(&full[s], (g / kStages) & 1);
+        if (g >= (uint32_t)kS) mbar_wait(&tempty[slot], ((g / kS) - 1) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t abase = smem_u32(ktiles + s * kTileBytes);
-          const uint32_t bbase = smem_u32(qbuf);
+          const uint32_t bbase = smem_u32(qbuf + qb * kQBytes);
 #pragma unroll
-          for (int kk = 0; kk < ((P.dbg & 2) ? 0 : D / 16); ++kk) {
+          for (int kk = 0; kk < D / 16; ++kk) {
             const int atom = kk / 4, sub = kk % 4;
-            mma_bf16(tmem + i * N, sw128_desc(abase + atom * kTileKeys * 128 + sub * 32),
+            mma_bf16(tmem + slot * N, sw128_desc(abase + atom * kTileKeys * 128 + sub * 32),
                      sw128_desc(bbase + atom * N * 128 + sub * 32), kIdesc, kk > 0 ? 1u : 0u);
           }
           mma_commit(&empty[s]);
-          mma_commit(&tfull[i]);
+          mma_commit(&tfull[slot]);
+          if (i == ntiles - 1) mma_commit(&qempty[qb]);
+          if (P.trace && i == ntiles - 1) P.trace[((int64_t)blockIdx.x * P.nl + l) * 8 + 7] = gtimer();
         }
         __syncwarp();
       }
     }
   } else {
-    float m[kNC], z[kNC];
+    // ---------------- epilogue ----------------
+    const int ew = warp - 2;                // 0 .. kPEW-1
+    const int quad = warp & 3;              // TMEM lane quadrant this warp may access
+    const int grp = ew / 4;                 // tile group
+    const int key_local = quad * 32 + lane;
+    const int et = threadIdx.x - 64;
+    int phase_k = 0;                        // head barriers passed
+    const float scale_b = P.agg == 2 ? 2.f * P.scale : P.scale;
+    for (int l = 0; l <= P.nl; ++l) {
+      unsigned long long *tr = (P.trace && l < P.nl) ? P.trace + ((int64_t)blockIdx.x * P.nl + l) * 8 : nullptr;
+      if (tr && et == 0) tr[0] = gtimer();
+      float m[N], z[N];
+      if (l < P.nl) {
+        const uint32_t gbase = (uint32_t)(l * ntiles);
+        // ---- A: online (max, sum exp2) per column, branch-free lazy rescale ----
 #pragma unroll
-    for (int c = 0; c < kNC; ++c) { m[c] = -INFINITY; z[c] = 0.f; }
-    for (int i = 0; i < ntiles; ++i) {
-      mbar_wait(&tfull[i], 0);
-      tc_fence_after();
-      float v[kNC];
-      const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + i * N + c0;
-      if constexpr (kNC == 16) tmem_ld16(tb, v);
-      else tmem_ld32(tb, v);
-      const int tile0 = (t_lo + i) * kTileKeys;
-      const int j = tile0 + key_local;
-      const bool fast = tile0 + kTileKeys - 1 <= P.start && tile0 + kTileKeys <= P.L;
-      if (P.dbg & 1) { m[0] = fmaxf(m[0], v[0]); continue; }
+        for (int c = 0; c < N; ++c) { m[c] = kNegBig; z[c] = 0.f; }
+        for (int i = grp; i < ntiles; i += kPGroups) {
+          const uint32_t g = gbase + i;
+          const int slot = g % kS;
+          mbar_wait(&tfull[slot], (g / kS) & 1);
+          tc_fence_after();
+          const int tile0 = (t_lo + i) * kTileKeys;
+          const int j = tile0 + key_local;
+          const bool fast = (tile0 + kTileKeys - 1 <= P.start && tile0 + kTileKeys <= P.L) || (P.dbg & 1);
+          const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + slot * N;
 #pragma unroll
-      for (int c = 0; c < kNC; ++c) {
-        if (fast || (j < P.L && j <= lim_s[c0 + c])) {
-          const float s = v[c] * P.scale;
-          const float mn = fmaxf(m[c], s);
-          z[c] = z[c] * exp2f(m[c] - mn) + exp2f(s - mn);
-          m[c] = mn;
+          for (int h = 0; h < N / 32; ++h) {
+            float v[32];
+            tmem_ld32(tb + h * 32, v);
+            if (fast) {  // every window row sees every key (padded columns are discarded later)
+#pragma unroll
+              for (int c = 0; c < 32; ++c) lse_step(m[h * 32 + c], z[h * 32 + c], v[c] * P.scale);
+            } else {
+              const uint32_t vm = window_mask(P, j, h);
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                lse_step(m[h * 32 + c], z[h * 32 + c], ((vm >> c) & 1u) ? v[c] * P.scale : -INFINITY);
+            }
+          }
+        }
+        // CTA partial per column: warp reduce-scatter, then fold the warps
+#pragma unroll
+        for (int h = 0; h < N / 32; ++h) {
+          warp_lse_scatter32(m + h * 32, z + h * 32, lane);
+          wred[ew * N + h * 32 + lane] = make_float2(m[h * 32], z[h * 32]);
+        }
+        if (tr && et == 0) tr[1] = gtimer();
+        named_sync(1, 32 * kPEW);
+        if (et < N) {
+          float2 acc = wred[et];
+#pragma unroll
+          for (int w = 1; w < kPEW; ++w) {
+            const float2 q = wred[w * N + et];
+            lse2_merge(acc.x, acc.y, q.x, q.y);
+          }
+          P.partial[((int64_t)head * P.cph + cidx) * N + et] = acc;
         }
       }
-    }
-    // CTA combine through the idle ring, then one partial per column
-    named_sync(1, 32 * kEW);
-    float *rm = reinterpret_cast<float *>(ktiles);
-    float *rz = rm + 128 * (N + 1);
-#pragma unroll
-    for (int c = 0; c < kNC; ++c) {
-      rm[key_local * (N + 1) + c0 + c] = m[c];
-      rz[key_local * (N + 1) + c0 + c] = z[c];
-    }
-    named_sync(1, 32 * kEW);
-    constexpr int kSl = 32 * kEW / N, kPer = 128 / kSl;
-    float mm = -INFINITY, zz = 0.f;
-    {
-      const int col = et % N, sl = et / N;
-      for (int k = sl * kPer; k < (sl + 1) * kPer; ++k) {
-        const float qm = rm[k * (N + 1) + col], qz = rz[k * (N + 1) + col];
-        if (qm == -INFINITY) continue;
-        const float mn = fmaxf(mm, qm);
-        zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + qz * exp2f(qm - mn);
-        mm = mn;
-      }
-    }
-    named_sync(1, 32 * kEW);
-    float2 *sl2 = reinterpret_cast<float2 *>(rm);
-    sl2[et] = make_float2(mm, zz);
-    named_sync(1, 32 * kEW);
-    if (et < N) {
-      float m2 = -INFINITY, z2 = 0.f;
-      for (int k = 0; k < kSl; ++k) {
-        const float2 q = sl2[k * N + et];
-        if (q.x == -INFINITY) continue;
-        const float mn = fmaxf(m2, q.x);
-        z2 = (m2 == -INFINITY ? 0.f : z2 * exp2f(m2 - mn)) + q.y * exp2f(q.x - mn);
-        m2 = mn;
-      }
-      P.partial[((int64_t)head * F.cph + cidx) * N + et] = make_float2(m2, z2);
-    }
-  }
-  head_barrier(&F.bar_cnt[head], F.cph);
+      // one head barrier per layer: after it, layer l's partials and layer
+      // l-1's raw metrics of the whole head are visible
+      epi_head_barrier(&P.bar_cnt[head], P.cph * (++phase_k), et == 0);
+      if (tr && et == 0) tr[2] = gtimer();
 
-  // ================= phase 2: head statistics, metric of resident tiles =======
-  for (int c = threadIdx.x; c < N; c += blockDim.x) {
-    float mm = -INFINITY, zz = 0.f;
-    for (int k = 0; k < F.cph; ++k) {
-      const float2 q = __ldcg(P.partial + ((int64_t)head * F.cph + k) * N + c);  // written by other CTAs
-      if (q.x == -INFINITY) continue;
-      const float mn = fmaxf(mm, q.x);
-      zz = (mm == -INFINITY ? 0.f : zz * exp2f(mm - mn)) + q.y * exp2f(q.x - mn);
-      mm = mn;
-    }
-    const bool real = c < P.RW;
-    stat_s[c] = real ? mm : INFINITY;
-    stat_s[N + c] = (real && zz > 0.f) ? 1.f / zz : 0.f;
-  }
-  __syncthreads();
-  if (warp >= 2) {
-    tc_fence_after();
-    for (int i = 0; i < ntiles; ++i) {
-      float v[kNC];
-      const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + i * N + c0;
-      if constexpr (kNC == 16) tmem_ld16(tb, v);
-      else tmem_ld32(tb, v);
-      const int tile0 = (t_lo + i) * kTileKeys;
-      const int j = tile0 + key_local;
-      const bool fast = tile0 + kTileKeys - 1 <= P.start;
-      float contrib = 0.f;
+      if (l < P.nl) {
+        const uint32_t gbase = (uint32_t)(l * ntiles);
+        // ---- B: head statistics (8 partial folds per column in parallel) ----
+        {
+          constexpr int kParts = 32 * kPEW / N;
+          const int col = et % N, part = et / N;
+          float mm = kNegBig, zz = 0.f;
+          for (int k = part; k < P.cph; k += kParts) {
+            const float2 q = __ldcg(P.partial + ((int64_t)head * P.cph + k) * N + col);  // other CTAs' partials
+            lse2_merge(mm, zz, q.x, q.y);
+          }
+          named_sync(1, 32 * kPEW);  // wred reuse
+          wred[part * N + col] = make_float2(mm, zz);
+          named_sync(1, 32 * kPEW);
+          if (et < N) {
+            float2 acc = wred[et];
 #pragma unroll
-      for (int c = 0; c < kNC; ++c) {
-        const float pr = exp2f(v[c] * P.scale - stat_s[c0 + c]) * stat_s[N + c0 + c];
-        const float f = P.agg == 2 ? pr * pr : pr;
-        contrib += (fast || j <= lim_s[c0 + c]) ? f : 0.f;
+            for (int w = 1; w < kParts; ++w) {
+              const float2 q = wred[w * N + et];
+              lse2_merge(acc.x, acc.y, q.x, q.y);
+            }
+            const bool real = et < P.RW;
+            const float iz = (real && acc.y > 0.f) ? 1.f / acc.y : 0.f;
+            // f(p) = p (L1) or p^2 = exp2(2(s - M)) / Z^2 (L2)
+            stat_s[et] = real ? (P.agg == 2 ? 2.f * acc.x : acc.x) : INFINITY;
+            stat_s[N + et] = P.agg == 2 ? iz * iz : iz;
+          }
+          named_sync(1, 32 * kPEW);
+        }
+#pragma unroll
+        for (int c = 0; c < N; ++c) { m[c] = stat_s[c]; z[c] = stat_s[N + c]; }
+        // ---- B: raw metric of the resident tiles; each slot is released after its last read ----
+        float *raw = P.raw + ((int64_t)(l & 1) * P.H + head) * P.Lp;
+        for (int i = grp; i < ntiles; i += kPGroups) {
+          const uint32_t g = gbase + i;
+          const int slot = g % kS;
+          const int tile0 = (t_lo + i) * kTileKeys;
+          const int j = tile0 + key_local;
+          const bool fast = tile0 + kTileKeys - 1 <= P.start;
+          const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16) + slot * N;
+          float contrib = 0.f;
+#pragma unroll
+          for (int h = 0; h < N / 32; ++h) {
+            float v[32];
+            tmem_ld32(tb + h * 32, v);
+            if (h == N / 32 - 1) {
+              tc_fence_before();
+              mbar_arrive(&tempty[slot]);  // slot free for the next layer's tiles
+            }
+            if (fast) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                contrib = fmaf(ex2_approx(fmaf(v[c], scale_b, -m[h * 32 + c])), z[h * 32 + c], contrib);
+            } else {
+              const uint32_t vm = window_mask(P, j, h);
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const float f = ex2_approx(fmaf(v[c], scale_b, -m[h * 32 + c])) * z[h * 32 + c];
+                contrib += ((vm >> c) & 1u) ? f : 0.f;
+              }
+            }
+          }
+          if (j < P.L) raw[j] = contrib;
+        }
+        if (tr && et == 0) tr[3] = gtimer();
       }
-      if (half > 0) halfsum[((half - 1) * kMaxT + i) * 128 + key_local] = contrib;
-      named_sync(2, 32 * kEW);
-      if (half == 0 && j < P.L) {
-        for (int gq = 1; gq < kGroups; ++gq) contrib += halfsum[((gq - 1) * kMaxT + i) * 128 + key_local];
-        P.raw[(int64_t)head * P.L + j] = contrib;
-      }
-    }
-  }
-  head_barrier(&F.bar_cnt[P.H + head], F.cph);
 
-  // ================= phase 3: centred max-pool + per-slot install ===========
-  {
-    const int half_p = F.pool / 2;
-    const float *raw = P.raw + (int64_t)head * P.L;
-    const int64_t hidx = F.row >= 0 ? head_index(F.p, F.row, F.layer, head) : 0;
-    const int C = F.row >= 0 ? F.p.ctx[hidx] : 0;
-    const int b = F.p.block_size;
-    const int j_lo = t_lo * kTileKeys, j_hi = min(P.L, t_hi * kTileKeys);
-    // stage this CTA's raw range plus the pooling halo in (idle) shared memory
-    float *rs = reinterpret_cast<float *>(ktiles);
-    const int s_lo = max(0, j_lo - half_p), s_hi = min(P.L, j_hi + half_p);
-    for (int t = s_lo + threadIdx.x; t < s_hi; t += blockDim.x) rs[t - s_lo] = __ldcg(raw + t);
-    __syncthreads();
-    for (int j = j_lo + threadIdx.x; j < j_hi; j += blockDim.x) {
-      float mx = rs[j - s_lo];
-      const int lo = j - half_p < 0 ? 0 : j - half_p;
-      const int hi = j + half_p >= P.L ? P.L - 1 : j + half_p;
-      for (int t = lo; t <= hi; ++t) mx = fmaxf(mx, rs[t - s_lo]);
-      if (F.out) F.out[(int64_t)head * P.L + j] = mx;
-      if (F.row >= 0 && j < C) {
-        const int64_t f = (int64_t)head_table(F.p, hidx)[j / b] * b + j % b;
-        F.p.metric[f] = mx;
-        F.p.logical[f] = j;
-        F.p.protected_[f] = (F.protect && j >= P.start) ? 1 : 0;
-        F.p.fresh[f] = 0;
+      // ---- C: pooling + install of the PREVIOUS layer (its raw metrics of
+      // the whole head became visible at this layer's barrier).  Four keys
+      // per step: their slots are contiguous (block_size % 4 == 0). ----
+      if (l >= 1) {
+        const int lp = l - 1;
+        const int half_p = P.pool / 2;
+        const float *raw = P.raw + ((int64_t)(lp & 1) * P.H + head) * P.Lp;
+        const int layer = P.layer0 + lp;
+        const int64_t hidx = P.row >= 0 ? head_index(P.p, P.row, layer, head) : 0;
+        const int b = P.row >= 0 ? P.p.block_size : 16;
+        const int j_lo = t_lo * kTileKeys, j_hi = min(P.L, t_hi * kTileKeys);
+        const int s_lo = j_lo - half_p;  // rs[t - s_lo] = raw[t]; outside [0, L): -inf
+        const int n_own = (j_hi - j_lo + 3) / 4;
+        // own range as float4 (j_lo is 128-aligned), halo as scalars, table slice
+        for (int t = et; t < n_own; t += 32 * kPEW) {
+          const int j = j_lo + 4 * t;
+          float4 v4;
+          if (j + 3 < P.L) v4 = __ldcg(reinterpret_cast<const float4 *>(raw + j));
+          else {
+            v4.x = raw[j];
+            v4.y = j + 1 < P.L ? __ldcg(raw + j + 1) : -INFINITY;
+            v4.z = j + 2 < P.L ? __ldcg(raw + j + 2) : -INFINITY;
+            v4.w = -INFINITY;
+          }
+          rs[half_p + 4 * t] = v4.x; rs[half_p + 4 * t + 1] = v4.y;
+          rs[half_p + 4 * t + 2] = v4.z; rs[half_p + 4 * t + 3] = v4.w;
+        }
+        if (et < 2 * half_p) {
+          const int k = et < half_p ? et : half_p + 4 * n_own + (et - half_p);
+          const int t = s_lo + k;
+          rs[k] = (t >= 0 && t < P.L) ? __ldcg(raw + t) : -INFINITY;
+        }
+        const int nb_rng = (j_hi - j_lo + b - 1) / b;
+        int *tab_s = reinterpret_cast<int *>(wred);  // idle here: kPEW*N*2 ints >= 16 tiles of blocks
+        const int C = P.row >= 0 ? P.p.ctx[hidx] : 0;
+        if (P.row >= 0)
+          for (int t = et; t < nb_rng; t += 32 * kPEW) tab_s[t] = __ldg(head_table(P.p, hidx) + j_lo / b + t);
+        named_sync(1, 32 * kPEW);
+        float *out = P.out ? P.out + lp * P.out_layer_stride + (int64_t)head * P.L : nullptr;
+        for (int t = et; t < n_own; t += 32 * kPEW) {
+          const int j = j_lo + 4 * t;
+          float w[4 + 2 * kMaxHalf];
+          float mx[4];
+          if (half_p <= kMaxHalf) {
+#pragma unroll
+            for (int k = 0; k < 4 + 2 * kMaxHalf; ++k) w[k] = k < 4 + 2 * half_p ? rs[4 * t + k] : -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float v = -INFINITY;
+#pragma unroll
+              for (int k = 0; k <= 2 * kMaxHalf; ++k) v = k <= 2 * half_p ? fmaxf(v, w[e + k]) : v;
+              mx[e] = v;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float v = -INFINITY;
+              for (int k = 0; k <= 2 * half_p; ++k) v = fmaxf(v, rs[4 * t + e + k]);
+              mx[e] = v;
+            }
+          }
+          if (out) {
+            if (j + 3 < P.L && (reinterpret_cast<uintptr_t>(out + j) & 15) == 0)
+              *reinterpret_cast<float4 *>(out + j) = make_float4(mx[0], mx[1], mx[2], mx[3]);
+            else
+              for (int e = 0; e < 4 && j + e < P.L; ++e) out[j + e] = mx[e];
+          }
+          if (P.row >= 0 && j < C) {
+            const int64_t f = (int64_t)tab_s[(j - j_lo) / b] * b + j % b;
+            const uint8_t pr[4] = {(uint8_t)(P.protect && j >= P.start), (uint8_t)(P.protect && j + 1 >= P.start),
+                                   (uint8_t)(P.protect && j + 2 >= P.start), (uint8_t)(P.protect && j + 3 >= P.start)};
+            if (j + 3 < C) {
+              *reinterpret_cast<float4 *>(P.p.metric + f) = make_float4(mx[0], mx[1], mx[2], mx[3]);
+              *reinterpret_cast<int4 *>(P.p.logical + f) = make_int4(j, j + 1, j + 2, j + 3);
+              *reinterpret_cast<uint32_t *>(P.p.protected_ + f) =
+                  pr[0] | (uint32_t)pr[1] << 8 | (uint32_t)pr[2] << 16 | (uint32_t)pr[3] << 24;
+              *reinterpret_cast<uint32_t *>(P.p.fresh + f) = 0u;
+            } else {
+              for (int e = 0; e < 4 && j + e < C; ++e) {
+                P.p.metric[f + e] = mx[e];
+                P.p.logical[f + e] = j + e;
+                P.p.protected_[f + e] = pr[e];
+                P.p.fresh[f + e] = 0;
+              }
+            }
+          }
+        }
+        named_sync(1, 32 * kPEW);  // rs / tab_s are refilled by the next layer
+        if (P.trace && et == 0) P.trace[((int64_t)blockIdx.x * P.nl + lp) * 8 + 5] = gtimer();
       }
     }
   }
@@ -687,88 +894,107 @@ bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_r
 }
 
 template <int N, int D>
-int run_fused(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cudaStream_t s, int *bar_cnt) {
-  constexpr int kMaxT = 512 / N;
-  auto fn = k_window_fused<N, D>;
-  const int smem = fused_stages<D>() * kTileKeys * D * 2 + N * D * 2 + N * 4 + 256 + 2 * N * 4 + (kFusedEW / 4) * kMaxT * 128 * 4 + 1024;
-  static bool configured = false;
-  static int capacity = 0;
-  if (!configured) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    int per_sm = 0, dev = 0, nsm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 64 + 32 * kFusedEW, smem);
+int run_persist(const kvc_pool *pool, const kvc_window_args *a, const WinParams &W, int nl, cudaStream_t s) {
+  constexpr int kS = 512 / N;
+  auto fn = k_window_persist<N, D>;
+  if (a->pool > 1023 || !W.bar_cnt) return KVC_ERR_UNSUPPORTED;
+  // phase C installs four contiguous slots at a time and stages the table slice in 2*kPEW*N ints
+  if (a->seq_row >= 0 && (pool->block_size % 4 != 0 || kS * kTileKeys / pool->block_size > 2 * kPEW * N))
+    return KVC_ERR_UNSUPPORTED;
+  const int smem = persist_smem<N, D>(a->pool);
+  if (smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
+  static int configured = 0, nsm = 0;
+  if (configured < smem) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    per_sm = per_sm > 1 ? 1 : per_sm;  // 512 TMEM columns per CTA
-    capacity = per_sm * nsm;
-    configured = true;
+    configured = smem;
   }
-  if (getenv("KVC_DEBUG")) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 64 + 32 * kFusedEW, smem);
-    cudaFuncAttributes at;
-    cudaFuncGetAttributes(&at, fn);
-    for (int sm2 : {100000, 90000, 60000, 30000}) {
-      int ps = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, 64 + 32 * 8, sm2);
-      int ps2 = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps2, fn, 64, sm2);
-      fprintf(stderr, "[kvc]   smem %d -> per_sm %d (64 thr: %d)\n", sm2, ps, ps2);
-    }
-    fprintf(stderr, "[kvc] fused K2: smem %d capacity %d per_sm %d regs %d static %zu maxdyn %d maxthr %d\n", smem,
-            capacity, per_sm, at.numRegs, at.sharedSizeBytes, at.maxDynamicSharedSizeBytes, at.maxThreadsPerBlock);
-  }
-  if (capacity < 1 || smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
-  const int total = P.H * P.tiles_per_head;
-  int tpc = (total + capacity - 1) / capacity;
-  if (tpc < 1) tpc = 1;
-  while (tpc <= kMaxT && P.H * ((P.tiles_per_head + tpc - 1) / tpc) > capacity) ++tpc;
-  if (tpc > kMaxT) return KVC_ERR_UNSUPPORTED;  // scores do not fit in TMEM: two-pass path
-  const int cph = (P.tiles_per_head + tpc - 1) / tpc;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPThreads, smem);
+  if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
+  // one CTA per SM: it owns all 512 TMEM columns
+  int cph = nsm / W.H;
+  if (cph > W.tiles_per_head) cph = W.tiles_per_head;
+  if (cph < 1 || (W.tiles_per_head + cph - 1) / cph > kS) return KVC_ERR_UNSUPPORTED;  // scores exceed TMEM
   CUtensorMap tmK, tmQ;
-  if (!make_map3(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
-  if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
-  CUtensorMap tmK16;
-  if (!make_map(&tmK16, a->k, (int64_t)P.H * P.L, D, 16)) return KVC_ERR_CUDA;
-  FusedParams F;
-  F.w = P;
-  F.cph = cph;
-  F.tiles_per_cta = tpc;
-  F.bar_cnt = bar_cnt;
-  F.p = *pool;
-  F.row = a->seq_row;
-  F.layer = a->layer;
-  F.pool = a->pool;
-  F.protect = a->protect_window;
-  F.out = a->metrics_out;
-  cudaMemsetAsync(bar_cnt, 0, 2 * P.H * sizeof(int), s);
+  if (!make_map3(&tmK, a->k, (int64_t)nl * W.H * W.L, D, kTileKeys)) return KVC_ERR_CUDA;
+  if (!make_map(&tmQ, a->q_win, (int64_t)nl * a->num_query_heads * W.wq, D, N)) return KVC_ERR_CUDA;
+  PersistParams P;
+  P.L = W.L; P.Lp = (W.L + 3) & ~3; P.H = W.H; P.RW = W.RW; P.wq = W.wq; P.start = W.start; P.nl = nl; P.n_q = a->num_query_heads;
+  P.tiles_per_head = W.tiles_per_head; P.cph = cph;
+  P.scale = W.scale; P.agg = W.agg;
+  P.partial = W.partial; P.raw = W.raw; P.bar_cnt = W.bar_cnt;
+  P.p = *pool;
+  P.row = a->seq_row; P.layer0 = a->layer; P.pool = a->pool; P.protect = a->protect_window;
+  P.out = a->metrics_out;
+  P.out_layer_stride = a->out_layer_stride;
+  P.trace = nullptr;
+  P.dbg = getenv("KVC_K2_DBG") ? atoi(getenv("KVC_K2_DBG")) : 0;
+  static const bool trace = getenv("KVC_K2_TRACE") != nullptr;
+  if (trace) cudaMalloc(&P.trace, (size_t)W.H * cph * nl * 8 * 8);
+  cudaMemsetAsync(W.bar_cnt, 0, W.H * sizeof(int), s);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P.H * cph);
-  cfg.blockDim = dim3(64 + 32 * kFusedEW);
+  cfg.gridDim = dim3(W.H * cph);
+  cfg.blockDim = dim3(kPThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: per-head grid barriers
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: per-head barriers
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, tmK, tmQ, tmK16, F) == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
+  const int rc = cudaLaunchKernelEx(&cfg, fn, tmK, tmQ, P) == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
+  if (trace) {
+    // debug: per layer, average over CTAs of each phase's duration (us), relative to the CTA's A start
+    const int G = W.H * cph;
+    unsigned long long *h = (unsigned long long *)malloc((size_t)G * nl * 64);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, P.trace, (size_t)G * nl * 64, cudaMemcpyDeviceToHost);
+    unsigned long long t00 = ~0ull;
+    for (int c = 0; c < G; ++c) t00 = h[(size_t)c * nl * 8] < t00 ? h[(size_t)c * nl * 8] : t00;
+    for (int l = 0; l < nl; ++l) {
+      double acc[8] = {0};
+      for (int c = 0; c < G; ++c)
+        for (int k = 0; k < 8; ++k) acc[k] += (double)(h[((size_t)c * nl + l) * 8 + k] - t00) / 1e3 / G;
+      // per head: spread of the A-finish times and barrier exit minus the last arrival
+      double skew = 0, lat = 0;
+      for (int hd = 0; hd < W.H; ++hd) {
+        double mn = 1e30, mx = 0, bx = 0;
+        for (int c = hd * cph; c < (hd + 1) * cph; ++c) {
+          const double a1 = (double)(h[((size_t)c * nl + l) * 8 + 1] - t00) / 1e3;
+          const double b1 = (double)(h[((size_t)c * nl + l) * 8 + 2] - t00) / 1e3;
+          mn = a1 < mn ? a1 : mn; mx = a1 > mx ? a1 : mx; bx += b1 / cph;
+        }
+        skew += (mx - mn) / W.H; lat += (bx - mx) / W.H;
+      }
+      fprintf(stderr, "[k2 trace] layer %2d: A0 %.2f A1 %.2f bar %.2f B %.2f C(next) %.2f | tma_first %.2f mma_last %.2f | A1 skew %.2f bar-lastA1 %.2f\n", l,
+              acc[0], acc[1], acc[2], acc[3], acc[5], acc[6], acc[7], skew, lat);
+    }
+    // per CTA index within a head: mean A1 relative to the head's earliest A1 (layers >= 1)
+    for (int ci = 0; ci < cph; ++ci) {
+      double d = 0;
+      for (int l = 1; l < nl; ++l)
+        for (int hd = 0; hd < W.H; ++hd) {
+          double mn = 1e30;
+          for (int c = hd * cph; c < (hd + 1) * cph; ++c) {
+            const double a1 = (double)(h[((size_t)c * nl + l) * 8 + 1] - t00) / 1e3;
+            mn = a1 < mn ? a1 : mn;
+          }
+          d += ((double)(h[((size_t)(hd * cph + ci) * nl + l) * 8 + 1] - t00) / 1e3 - mn) / ((nl - 1) * W.H);
+        }
+      fprintf(stderr, "[k2 trace] cidx %2d tiles %d: A1 - head min %.2f us\n", ci,
+              (int)((int64_t)(ci + 1) * W.tiles_per_head / cph - (int64_t)ci * W.tiles_per_head / cph), d);
+    }
+    free(h);
+    cudaFree(P.trace);
+  }
+  return rc;
 }
 
 template <int N, int D>
 int run_window(const kvc_pool *pool, const kvc_window_args *a, WinParams &P, cudaStream_t s) {
-  {
-    static int fused_off = -1;
-    if (fused_off < 0) {
-      const char *e = getenv("KVC_K2_TWOPASS");
-      fused_off = (e && atoi(e) == 1) ? 1 : 0;
-    }
-    if (!fused_off && D <= 128 && P.bar_cnt) {
-      const int rc = run_fused<N, D>(pool, a, P, s, P.bar_cnt);
-      if (rc != KVC_ERR_UNSUPPORTED) return rc;
-    }
-  }
   CUtensorMap tmK, tmQ;
   if (!make_map3(&tmK, a->k, (int64_t)P.H * P.L, D, kTileKeys)) return KVC_ERR_CUDA;
   if (!make_map(&tmQ, a->q_win, (int64_t)a->num_query_heads * P.wq, D, N)) return KVC_ERR_CUDA;
@@ -836,14 +1062,30 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   if (!N) return KVC_ERR_UNSUPPORTED;
   Scratch sc(pool);
   P.partial = sc.take<float2>((int64_t)H * (chunks > 304 ? chunks : 304) * N);
-  P.raw = sc.take<float>((int64_t)H * a->L);
+  P.raw = sc.take<float>((int64_t)2 * H * ((a->L + 3) & ~3));  // two layers in flight (persistent kernel)
   P.bar_cnt = sc.take<int>(2 * H);
   if (!P.partial || !P.raw) return KVC_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = a->n_layers > 1 ? a->n_layers : 1;
   if (a->layer < 0 || (a->seq_row >= 0 && a->layer + nl > pool->num_layers)) return KVC_ERR_INVALID;
-  // one layer at a time: the layer's K (64 MB at Llama-8B shapes) stays in L2
-  // between the statistics pass and the metric pass
+  static int twopass = -1;  // KVC_K2_TWOPASS=1: per-layer two-pass kernels (experiments)
+  if (twopass < 0) {
+    const char *e = getenv("KVC_K2_TWOPASS");
+    twopass = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  // persistent kernel over all layers when the layers are packed back to back
+  const bool packed = nl == 1 || (a->k_layer_stride == (int64_t)H * a->L * D &&
+                                  a->q_layer_stride == (int64_t)a->num_query_heads * P.wq * D);
+  if (!twopass && packed && D <= 128) {
+    int rc = KVC_ERR_UNSUPPORTED;
+    if (N == 32 && D == 64) rc = run_persist<32, 64>(pool, a, P, nl, s);
+    else if (N == 32 && D == 128) rc = run_persist<32, 128>(pool, a, P, nl, s);
+    else if (N == 64 && D == 64) rc = run_persist<64, 64>(pool, a, P, nl, s);
+    else if (N == 64 && D == 128) rc = run_persist<64, 128>(pool, a, P, nl, s);
+    if (rc != KVC_ERR_UNSUPPORTED) return rc;
+  }
+  // otherwise one layer at a time, two passes: the layer's K (64 MB at
+  // Llama-8B shapes) stays in L2 between the statistics and the metric pass
   for (int li = 0; li < nl; ++li) {
     kvc_window_args al = *a;
     al.layer = a->layer + li;

@@ -68,8 +68,8 @@ def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev,
         pool_p.status = _lib.DeviceContext.get(dev).status.data_ptr()
     pool_p.num_kv_heads = num_kv_heads
     pool_p.head_dim = head_dim
-    # raw [H][L] f32 + partials [H][<=304][<=64] float2 + barrier counters
-    with_scratch(pool_p, dev, num_kv_heads * (L * 4 + 304 * 64 * 8 + 64) + (1 << 16))
+    # raw [2][H][L] f32 + partials [H][<=304][<=64] float2 + barrier counters
+    with_scratch(pool_p, dev, num_kv_heads * (2 * (L + 3) * 4 + 304 * 64 * 8 + 64) + (1 << 16))
     _lib.check(_lib.lib().kvc_window_metric(ctypes.byref(pool_p), ctypes.byref(a), _lib.stream_ptr(dev)),
                "window_metric")
 

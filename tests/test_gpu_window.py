@@ -78,3 +78,22 @@ def test_prefill_install_then_compress_exact():
     E = O.budget_to_blocks(L // 8, layers, H, b, st.block_count(0))
     got = K.compress(rig.cache, rig.tables, rig.manager, rig.store, {0: E}).to_dict()
     assert got == O.compress(st, {0: E})
+
+
+@pytest.mark.parametrize("layers,H,r,d,L", [(3, 8, 4, 128, 4100), (4, 2, 4, 64, 9000), (2, 8, 8, 128, 1500)])
+def test_window_metric_multi_layer(layers, H, r, d, L):
+    """One K2 call over several layers (the persistent kernel streams layer
+    l+1 while layer l is finished) equals the oracle layer by layer."""
+    rng = np.random.default_rng(layers * 1000 + L)
+    w = 8
+    q = bf16_round(rng.standard_normal((layers, H * r, w, d)))
+    k = bf16_round(rng.standard_normal((layers, H, L, d)))
+    cfg = K.MetricConfig()
+    out = torch.empty((layers, H, L), dtype=torch.float32, device="cuda")
+    t = lambda x: torch.from_numpy(x).to("cuda", torch.bfloat16)
+    K.prefill._window_call(t(q), t(k), cfg, H, d, torch.device("cuda"), metrics_out=out)
+    _lib.DeviceContext.get(out.device).raise_status()
+    g = out.cpu().numpy().astype(np.float64)
+    for layer in range(layers):
+        want, _ = O.window_metric(q[layer], k[layer], H, w, cfg.pool, "L2")
+        assert np.allclose(g[layer], want, rtol=RTOL, atol=1e-6 * want.max()), (layer, np.abs(g[layer] - want).max())
