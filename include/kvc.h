@@ -147,6 +147,13 @@ int kvc_append_kv(const kvc_pool *pool, const int32_t *heads, const void *k,
 int kvc_write_prefill_kv(const kvc_pool *pool, int32_t seq_row, int32_t layer,
                          const void *k, const void *v, int32_t L, void *stream);
 
+/* The same for n_layers consecutive layers (layer, layer+1, ...) in one
+ * launch; k/v bf16 [n_layers][heads][L][head_dim] (engine.py:340-348 loops
+ * the layers of a prompt). */
+int kvc_write_prefill_kv_layers(const kvc_pool *pool, int32_t seq_row, int32_t layer,
+                                int32_t n_layers, const void *k, const void *v, int32_t L,
+                                void *stream);
+
 /* Install prompt metrics for one (row, layer): metrics f32 [heads][L],
  * protected u8 [L] (nullable = none); logical := position, fresh := 0. */
 int kvc_write_prompt_pass(const kvc_pool *pool, int32_t seq_row, int32_t layer,

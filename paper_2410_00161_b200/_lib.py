@@ -87,6 +87,7 @@ _SIGS = {
     "kvc_free_sequence": ([_p, _i32, _p], _i32),
     "kvc_append_kv": ([_p, _p, _p, _p, _i32, _i32, _p], _i32),
     "kvc_write_prefill_kv": ([_p, _i32, _i32, _p, _p, _i32, _p], _i32),
+    "kvc_write_prefill_kv_layers": ([_p, _i32, _i32, _i32, _p, _p, _i32, _p], _i32),
     "kvc_write_prompt_pass": ([_p, _i32, _i32, _p, _i64, _p, _i32, _p], _i32),
     "kvc_paged_decode": ([_p, _p, _p], _i32),
     "kvc_decode_scratch_bytes": ([_p, _i32, _i32, _i32], _i64),

@@ -529,21 +529,43 @@ __global__ void k_clear_fresh_rows(kvc_pool p, const int32_t *rows, int n_rows) 
   p.fresh[slot] = 0;
 }
 
-// K/V scatter of a prompt: vectorised 16-byte copies, table-mapped slots.
-__global__ void k_write_prefill_kv(kvc_pool p, int row, int layer, const uint4 *k, const uint4 *v, int L) {
+// K/V scatter of a prompt: a warp copies one table block (b rows, contiguous
+// on both sides: the prompt's rows [blk*b, blk*b + b) and the pool block),
+// 16 bytes per lane, four chunks in flight; 32-bit index math per block.
+__global__ void __launch_bounds__(256) k_write_prefill_kv(kvc_pool p, int row, int layer0, const uint4 *k,
+                                                          const uint4 *v, int L) {
   const int head = blockIdx.y;
+  const int layer = layer0 + blockIdx.z;
+  k += (int64_t)blockIdx.z * gridDim.y * L * (p.head_dim / 8);  // [layer][heads][L][d]
+  v += (int64_t)blockIdx.z * gridDim.y * L * (p.head_dim / 8);
   const int64_t hidx = head_index(p, row, layer, head);
   const int b = p.block_size;
-  const int vec = p.head_dim / 8;
+  const int vec = p.head_dim / 8;  // 16-byte chunks per row
+  const int nblk = (L + b - 1) / b;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int32_t *tab = head_table(p, hidx);
+  const uint4 *ks = k + (int64_t)head * L * vec;
+  const uint4 *vs = v + (int64_t)head * L * vec;
   uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
   uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
-  const int64_t n = (int64_t)L * vec;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int pos = (int)(e / vec);
-    const int64_t slot = (int64_t)tab[pos / b] * b + pos % b;
-    kc[slot * vec + e % vec] = k[(int64_t)head * n + e];
-    vc[slot * vec + e % vec] = v[(int64_t)head * n + e];
+  for (int bl = blockIdx.x * 8 + warp; bl < nblk; bl += gridDim.x * 8) {
+    const int rows = min(b, L - bl * b);
+    const int n = rows * vec;  // chunks of this block
+    const uint4 *sk = ks + (int64_t)bl * b * vec, *sv = vs + (int64_t)bl * b * vec;
+    const int64_t d0 = (int64_t)tab[bl] * b * vec;
+    for (int c0 = 0; c0 < n; c0 += 4 * 32) {
+      uint4 tk[4], tv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < n) { tk[u] = __ldcs(sk + c); tv[u] = __ldcs(sv + c); }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < n) { kc[d0 + c] = tk[u]; vc[d0 + c] = tv[u]; }
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ctx[hidx] = L;
 }
@@ -667,18 +689,28 @@ int kvc_clear_fresh(const kvc_pool *pool, const int32_t *seq_rows, int32_t n_row
   return KVC_OK;
 }
 
-int kvc_write_prefill_kv(const kvc_pool *pool, int32_t seq_row, int32_t layer, const void *k, const void *v,
-                         int32_t L, void *stream) {
-  if (!pool || !k || !v || L < 0 || pool->head_dim % 8 != 0) return KVC_ERR_INVALID;
+int kvc_write_prefill_kv_layers(const kvc_pool *pool, int32_t seq_row, int32_t layer, int32_t n_layers,
+                                const void *k, const void *v, int32_t L, void *stream) {
+  if (!pool || !k || !v || L < 0 || n_layers < 1 || pool->head_dim % 8 != 0 || pool->block_size < 1)
+    return KVC_ERR_INVALID;
+  if (layer < 0 || layer + n_layers > pool->num_layers) return KVC_ERR_INVALID;
   if (L == 0) return KVC_OK;
-  const int64_t n = (int64_t)L * (pool->head_dim / 8);
-  int gx = (int)((n + 255) / 256);
-  if (gx > 1184) gx = 1184;
-  dim3 grid(gx, pool->num_kv_heads);
+  const int nblk = (L + pool->block_size - 1) / pool->block_size;
+  int gx = (nblk + 7) / 8;  // 8 warps per CTA, one block per warp
+  const int H = pool->num_kv_heads > 0 ? pool->num_kv_heads : 1;
+  int cap = 148 * 16 / (H * n_layers);
+  if (cap < 1) cap = 1;
+  if (gx > cap) gx = cap;
+  dim3 grid(gx, pool->num_kv_heads, n_layers);
   k_write_prefill_kv<<<grid, 256, 0, (cudaStream_t)stream>>>(*pool, seq_row, layer, (const uint4 *)k,
                                                              (const uint4 *)v, L);
   KVC_CHECK_LAUNCH();
   return KVC_OK;
+}
+
+int kvc_write_prefill_kv(const kvc_pool *pool, int32_t seq_row, int32_t layer, const void *k, const void *v,
+                         int32_t L, void *stream) {
+  return kvc_write_prefill_kv_layers(pool, seq_row, layer, 1, k, v, L, stream);
 }
 
 int kvc_write_prompt_pass(const kvc_pool *pool, int32_t seq_row, int32_t layer, const float *metrics,

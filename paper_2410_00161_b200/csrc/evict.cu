@@ -49,6 +49,7 @@ struct EvictState {
   int32_t *lec;       // [T] keys <= T*
   // per sequence
   int32_t *R;         // [n_seqs][kBins] contribution deltas per digit
+  int32_t *done;      // [n_seqs] heads finished in the current histogram kernel (last one finds the digit)
   uint32_t *prefix;   // [n_seqs] T* digits found so far
   int64_t *E;         // [n_seqs] clamped budget (0 = inactive)
   int64_t *seq_moves; // [n_seqs] move slots of the sequence, then its base offset
@@ -112,10 +113,86 @@ __device__ void add_contrib(const int32_t *cum, int32_t base, int cap, int b, in
   }
 }
 
+// (2/4/6) per sequence: clamp E, find the first digit whose cumulative row
+// count reaches E, append it to the prefix, reset R.  Run by the last CTA of
+// the sequence to finish the preceding histogram kernel (NT threads).
+template <int NT>
+__device__ void find_digit(const int64_t *req, EvictState &S, int si, int level, int bits, int64_t *clamped) {
+  using Scan = cub::BlockScan<int32_t, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int found;
+  int32_t *R = S.R + (int64_t)si * kBins;
+  const int nbins = 1 << bits;
+  if (level == 1) {
+    // level 1 also computes the clamp: R summed over all bins = sum cap
+    if (req[si] <= 0) {
+      if (threadIdx.x == 0) { S.E[si] = 0; clamped[si] = req[si]; }  // min(req, sum cap) = req
+      for (int c = threadIdx.x; c < kBins; c += NT) R[c] = 0;
+      return;
+    }
+  } else if (S.E[si] <= 0) {
+    return;
+  }
+  constexpr int per = kBins / NT;
+  int32_t v[per];
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    const int c = threadIdx.x * per + i;
+    v[i] = c < nbins ? __ldcg(R + c) : 0;  // accumulated by other CTAs' atomics
+    s += v[i];
+  }
+  int32_t excl, total;
+  Scan(tmp).ExclusiveSum(s, excl, total);
+  if (threadIdx.x == 0) found = kBins;
+  __syncthreads();
+  const int64_t E = level == 1 ? (req[si] < total ? req[si] : total) : S.E[si];  // min(requested, sum cap)
+  if (E > 0) {
+    int32_t run = excl;
+#pragma unroll
+    for (int i = 0; i < per; ++i) {
+      run += v[i];
+      const int c = threadIdx.x * per + i;
+      if (c < nbins && run >= E) { atomicMin(&found, c); break; }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kBins; c += NT) R[c] = 0;
+  if (threadIdx.x == 0 && E > 0 && found >= nbins) set_status(S.status, KVC_DEV_SCHEDULE_CORRUPTION, si, level);
+  if (threadIdx.x == 0) {
+    if (level == 1) {
+      S.E[si] = E;
+      clamped[si] = E;
+      S.prefix[si] = (uint32_t)found;
+    } else {
+      S.prefix[si] = (S.prefix[si] << bits) | (uint32_t)found;
+    }
+  }
+}
+
+// True in every thread of the CTA that is the last of sequence si's heads to
+// arrive (its contributions and everyone else's are then visible); that CTA
+// also re-arms the counter for the next kernel.
+__device__ __forceinline__ bool last_of_sequence(EvictState &S, int si) {
+  __shared__ int last_s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(&S.done[si], 1);
+    last_s = prev == S.hp - 1;
+    if (last_s) {
+      S.done[si] = 0;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return last_s != 0;
+}
+
 // (1) keys + cap + level-1 histogram contributions.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
-                                                  EvictState S, int with_hist) {
+                                                  EvictState S, int with_hist, int64_t *clamped) {
   __shared__ int32_t hist[kBins];
   __shared__ int32_t shield_s;
   const int g = blockIdx.x;
@@ -129,6 +206,7 @@ __global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, co
   uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
   if (n > S.max_slots) {
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_CAPACITY, (int32_t)hidx, (int32_t)n);
+    if (with_hist && last_of_sequence(S, si)) find_digit<NT>(req, S, si, 1, 11, clamped);
     return;
   }
   for (int i = threadIdx.x; i < kBins; i += NT) hist[i] = 0;
@@ -192,77 +270,19 @@ __global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, co
   int cap = nb - (sh_blocks > 1 ? sh_blocks : 1);
   if (cap < 0) cap = 0;
   if (threadIdx.x == 0) S.cap[g] = cap;
-  if (!with_hist || req[si] <= 0) return;
-  scan_hist<NT>(hist);
-  add_contrib<NT>(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
-}
-
-// (2/4/6) per sequence: clamp E, find the first digit whose cumulative row
-// count reaches E, append it to the prefix, reset R.
-__global__ void __launch_bounds__(1024) k_find(const int64_t *req, EvictState S, int level, int bits,
-                                              int64_t *clamped) {
-  using Scan = cub::BlockScan<int32_t, 1024>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int found;
-  const int si = blockIdx.x;
-  int32_t *R = S.R + (int64_t)si * kBins;
-  const int nbins = 1 << bits;
-  if (level == 1) {
-    // level 1 also computes the clamp: R summed over all bins = sum cap
-    if (req[si] <= 0) {
-      if (threadIdx.x == 0) { S.E[si] = 0; clamped[si] = req[si]; }  // min(req, sum cap) = req
-      for (int c = threadIdx.x; c < kBins; c += 1024) R[c] = 0;
-      return;
-    }
-  } else if (S.E[si] <= 0) {
-    return;
+  if (!with_hist) return;
+  if (req[si] > 0) {
+    scan_hist<NT>(hist);
+    add_contrib<NT>(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
   }
-  constexpr int per = kBins / 1024;
-  int32_t v[per];
-  int32_t s = 0;
-#pragma unroll
-  for (int i = 0; i < per; ++i) {
-    const int c = threadIdx.x * per + i;
-    v[i] = c < nbins ? R[c] : 0;
-    s += v[i];
-  }
-  int32_t excl, total;
-  Scan(tmp).ExclusiveSum(s, excl, total);
-  if (threadIdx.x == 0) found = kBins;
-  __syncthreads();
-  int64_t E;
-  if (level == 1) {
-    E = req[si] < total ? req[si] : total;  // min(requested, sum cap)
-  } else {
-    E = S.E[si];
-  }
-  if (E > 0) {
-    int32_t run = excl;
-#pragma unroll
-    for (int i = 0; i < per; ++i) {
-      run += v[i];
-      const int c = threadIdx.x * per + i;
-      if (c < nbins && run >= E) { atomicMin(&found, c); break; }
-    }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < kBins; c += 1024) R[c] = 0;
-  if (threadIdx.x == 0 && E > 0 && found >= nbins) set_status(S.status, KVC_DEV_SCHEDULE_CORRUPTION, si, level);
-  if (threadIdx.x == 0) {
-    if (level == 1) {
-      S.E[si] = E;
-      clamped[si] = E;
-      S.prefix[si] = (uint32_t)found;
-    } else {
-      S.prefix[si] = (S.prefix[si] << bits) | (uint32_t)found;
-    }
-  }
+  if (last_of_sequence(S, si)) find_digit<NT>(req, S, si, 1, 11, clamped);
 }
 
 // (3/5) per head: histogram of the next digit among keys matching the prefix.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
-                                                  int shift, int bits) {
+                                                  int shift, int bits, const int64_t *req, int level,
+                                                  int64_t *clamped) {
   __shared__ int32_t hist[kBins];
   __shared__ int64_t below_s;
   const int g = blockIdx.x;
@@ -296,6 +316,7 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
   __syncthreads();
   scan_hist<NT>(hist);
   add_contrib<NT>(hist, (int32_t)below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
+  if (last_of_sequence(S, si)) find_digit<NT>(req, S, si, level, bits, clamped);
 }
 
 // (7) per head: rows with threshold < T* and <= T*.  With S.cand, also the
@@ -767,7 +788,7 @@ __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
+__global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
   extern __shared__ uint32_t bitmap[];  // [words] bitmap + [words] prefix
   __shared__ int32_t hist[kBins];
   __shared__ int32_t cnt_s[4];
@@ -812,12 +833,19 @@ __global__ void __launch_bounds__(NT) k_compact16(kvc_pool p, const int32_t *row
   if (tie_rank + 1 < tie_cnt) {
     int64_t dummy, dummy2;
     Sx = select16<NT>(hist, n, tie_rank, [&](int64_t pos, uint32_t *v, bool *ok) {
+      const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);  // pos % 4 == 0, rows padded to 4
+      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+      bool any = false;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int64_t ps = pos + i;
-        ok[i] = ps < n && keys[ps] == T;
-        v[i] = ok[i] ? sec(ps, p.logical[(int64_t)tab[ps / 16] * 16 + ps % 16]) : 0u;
+        ok[i] = pos + i < n && kv[i] == T;
+        any |= ok[i];
       }
+      int4 l4 = make_int4(0, 0, 0, 0);
+      if (any) l4 = *reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[pos / 16] * 16 + pos % 16);
+      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = ok[i] ? sec(pos + i, lv[i]) : 0u;
     }, &dummy, &dummy2);
   }
 
@@ -939,8 +967,21 @@ __global__ void __launch_bounds__(NT) k_compact16(kvc_pool p, const int32_t *row
     *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
     *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
     p.free_flag[blk] = 1;
-    atomicAdd(&p.free_tile[blk / KVC_FREE_TILE], 1);
     if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
+  }
+  {
+    // free-tile counts: one atomic per (warp, tile) instead of per block
+    // (a head's blocks sit in a few tiles, so per-block atomics serialise)
+    for (int base = 0; base < e; base += NT) {
+      const int t = base + threadIdx.x;
+      const bool act = t < e;
+      const unsigned am = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const int tile = tab[rb + t] / KVC_FREE_TILE;
+        const unsigned peers = __match_any_sync(am, tile);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&p.free_tile[tile], __popc(peers));
+      }
+    }
   }
   const int keep = rb;
   const int Cn = C < keep * 16 ? C : keep * 16;
@@ -1604,12 +1645,13 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.ltc = sc.take<int32_t>(T);
   S.lec = sc.take<int32_t>(T);
   S.R = sc.take<int32_t>((int64_t)a->n_seqs * kBins);
+  S.done = sc.take<int32_t>(a->n_seqs);
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
   S.seq_moves = sc.take<int64_t>(a->n_seqs);
   // candidate lists for the warp-per-head compaction of short heads
   S.cand = small_heads(S) && pool->block_size == 16 ? sc.take<unsigned long long>(T * 2 * kCand) : nullptr;
-  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.prefix || !S.E || !S.seq_moves ||
+  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.done || !S.prefix || !S.E || !S.seq_moves ||
       (small_heads(S) && pool->block_size == 16 && !S.cand))
     return KVC_ERR_INVALID;
   return KVC_OK;
@@ -1626,23 +1668,20 @@ int validate(const kvc_pool *pool, const kvc_evict_args *a) {
 int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
   const int64_t T = (int64_t)a->n_seqs * S.hp;
   cudaMemsetAsync(S.R, 0, (int64_t)a->n_seqs * kBins * sizeof(int32_t), s);
+  cudaMemsetAsync(S.done, 0, (int64_t)a->n_seqs * sizeof(int32_t), s);
+  // three radix levels (11 + 11 + 10 bits); the last head CTA of each
+  // sequence finds that level's digit inside the histogram kernel
   if (small_heads(S)) {
     constexpr int NT = 256;
-    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1);
-    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 1, 11, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11);
-    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 2, 11, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10);
-    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 3, 10, a->clamped);
+    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3, a->clamped);
     k_bounds<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S);
   } else {
     constexpr int NT = kThreads;
-    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1);
-    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 1, 11, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11);
-    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 2, 11, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10);
-    k_find<<<a->n_seqs, 1024, 0, s>>>(a->budgets, S, 3, 10, a->clamped);
+    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2, a->clamped);
+    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3, a->clamped);
     k_bounds<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S);
   }
   if (a->n_seqs > 0) {
@@ -1668,13 +1707,14 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
   if (pool->block_size == 16) {
     static bool conf16 = false;
     if (!conf16) {
-      cudaFuncSetAttribute(k_compact16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_compact16<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
       conf16 = true;
     }
     if (small_heads(S)) {
       k_compact_warp<<<(unsigned)((T + kWC - 1) / kWC), kWC * 32, 0, s>>>(*pool, a->seq_rows, S, M, T);
     }
-    else k_compact16<1024><<<(int)T, 1024, dyn, s>>>(*pool, a->seq_rows, S, M);
+    else if (dyn <= 100 * 1024) k_compact16<512><<<(int)T, 512, dyn, s>>>(*pool, a->seq_rows, S, M);
+    else return KVC_ERR_UNSUPPORTED;
   } else {
     k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
   }
@@ -1717,8 +1757,8 @@ int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *a, void *strea
   cudaStream_t s = (cudaStream_t)stream;
   // keys are recomputed so the call is self-contained
   const int64_t T = (int64_t)a->n_seqs * S.hp;
-  if (small_heads(S)) k_load<256><<<(int)T, 256, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0);
-  else k_load<kThreads><<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0);
+  if (small_heads(S)) k_load<256><<<(int)T, 256, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0, a->clamped);
+  else k_load<kThreads><<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0, a->clamped);
   return run_compact(pool, a, S, s);
 }
 

@@ -106,6 +106,19 @@ def write_prefill_kv(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, la
     tables.ctx_bound[row] = max(tables.ctx_bound[row], L)
 
 
+def write_prefill_kv_layers(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, k, v) -> None:
+    """Scatter every layer's prompt K/V (layers, heads, L, d) in one launch; C := L."""
+    dev = cache.device
+    kt, vt = _dev_bf16(k, dev), _dev_bf16(v, dev)
+    nl, L = kt.shape[0], kt.shape[2]
+    p = pool_struct(cache=cache, tables=tables)
+    _lib.check(_lib.lib().kvc_write_prefill_kv_layers(ctypes.byref(p), tables.row(seq_id), 0, nl, kt.data_ptr(),
+                                                      vt.data_ptr(), L, _lib.stream_ptr(dev)),
+               "write_prefill_kv_layers")
+    row = tables.row(seq_id)
+    tables.ctx_bound[row] = max(tables.ctx_bound[row], L)
+
+
 def prefill_layer(cache: UnifiedKVCache, tables: BlockTables, store: MetricsStore, seq_id: int, layer: int,
                   q, k, v, cfg: MetricConfig) -> None:
     """One layer of the engine prefill: scatter K/V, window metric, install
@@ -134,8 +147,7 @@ def prefill_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockM
     L = k.shape[2]
     demand = manager.allocate_prefill(seq_id, L)
     kt, vt, qt = _dev_bf16(k, dev), _dev_bf16(v, dev), _dev_bf16(q, dev)
-    for layer in range(tables.num_layers):
-        write_prefill_kv(cache, tables, seq_id, layer, kt[layer], vt[layer])
+    write_prefill_kv_layers(cache, tables, seq_id, kt, vt)
     p = pool_struct(cache=cache, tables=tables, store=store)
     _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
                  seq_row=tables.row(seq_id), layer=0)
