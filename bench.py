@@ -153,7 +153,7 @@ def build(args, dev, rank):
     num_blocks = int(B * (per_seq_blocks * 1.25 + growth) + nb_prefill + 4096)
     max_blocks = -(-L // b) + 8
     cache = K.UnifiedKVCache(num_blocks, b, d, device=dev)
-    tables = K.BlockTables(l, H, b, max_seqs=B + 1, max_blocks=max_blocks, device=dev)
+    tables = K.BlockTables(l, H, b, max_seqs=B + 2, max_blocks=max_blocks, device=dev)
     manager = K.BlockManager(num_blocks, tables)
     store = K.MetricsStore(num_blocks, b, device=dev)
     cfg = K.AttentionConfig(n_q, H, d, l)
@@ -205,6 +205,24 @@ def eviction_rounds(S, args):
         out["freed"].append(tot[0])
         out["evicted"].append(tot[1])
         out["moves"].append(tot[2])
+    # the same prefill + compress fused (kvc_prefill_compress): evicted rows are
+    # never written and survivors never moved; a spare table row, freed after
+    out["fused_ms"] = []
+    for i in range(args.prefill_seqs):
+        sid = 1_000_000 + i
+        q = torch.randn((l, S["n_q"], 8, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        k = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        v = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        E = K.budget_to_blocks(S["keep_tokens"], l, H, b, l * H * -(-L // b))
+        e0, e1 = ev(), ev()
+        torch.cuda.synchronize()
+        K.prefill_compress_sequence(cache, tables, manager, store, sid, q, k, v, S["mcfg"], E, sync=False,
+                                    events=(e0, e1))
+        torch.cuda.synchronize()
+        S["_lib"].DeviceContext.get(dev).raise_status()
+        out["fused_ms"].append(e0.elapsed_time(e1))
+        del k, v
+        manager.free_sequence(sid, store=store)
     return out
 
 
@@ -560,6 +578,11 @@ def main():
                             "total": (k2 or 0) + (k34 or 0), "kv_scatter_not_counted": float(np.mean(ev["scatter_ms"][timed]))},
         "freed_blocks": ev["freed"], "moves": ev["moves"], "evicted_kvs": ev["evicted"],
         "rounds_ms": {"k2": ev["k2_ms"], "k3k4": ev["k34_ms"], "first_round_is_warmup": len(ev["k2_ms"]) > 1},
+        "prefill_side_per_sequence_ms": {
+            "what": "prompt K/V into the cache + window metric + compress to the budget, per new sequence",
+            "unfused_scatter_k2_k3k4": float(np.mean(ev["scatter_ms"][timed])) + (k2 or 0) + (k34 or 0),
+            "fused_prefill_compress": float(np.mean(ev["fused_ms"][timed])) if ev["fused_ms"] else None,
+            "fused_rounds_ms": ev["fused_ms"]},
         "ratio_to_decode_step": {
             "raw_with_k2": ((k2 or 0) + (k34 or 0)) / step_ms, "raw_without_k2": (k34 or 0) / step_ms,
             "amortised_500_tokens_with_k2": ((k2 or 0) + (k34 or 0)) * B / 500 / step_ms},

@@ -32,6 +32,7 @@
  *   kvc_schedule_evictions  build_views .. eviction_mask      compression.py:122-231
  *   kvc_execute_moves       move_cache + free_schedule_blocks compression.py:234-309
  *   kvc_compress            compress (both of the above)      compression.py:312-355
+ *   kvc_prefill_compress    prefill scatter + compress fused  engine.py:340-358 + compression.py:312-355
  *   kvc_clear_fresh         MetricsStore.clear_fresh          metrics.py:185-186
  */
 #ifndef KVC_H_
@@ -244,6 +245,10 @@ typedef struct kvc_evict_args {
   int64_t *move_offsets;    /* [n_seqs*layers*heads + 1] exclusive prefix of e*b */
   int32_t *move_counts;     /* [n_seqs][layers*heads] */
   int64_t *totals;          /* [4]: freed blocks, evicted kvs, moves, free count */
+  /* NULL, or [n_seqs*layers*heads][max_slots_per_head]: for each kept
+   * position after compaction, the logical it held before renumbering
+   * (-1 = empty); written by kvc_prefill_compress's compaction */
+  int32_t *src_pos;
 } kvc_evict_args;
 
 /* Per-head evicted block counts (schedule_evictions); no state mutation. */
@@ -256,6 +261,17 @@ int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *args, void *st
 /* schedule_evictions + execute_moves in one pass over the slots (the
  * reference's compress, compression.py:312-355). */
 int kvc_compress(const kvc_pool *pool, const kvc_evict_args *args, void *stream);
+
+/* Compress a prompt that was allocated and scored (kvc_window_metric with
+ * seq_row) but whose K/V was never scattered: schedule + compaction on the
+ * slot metadata, then each surviving prompt row is written straight to its
+ * final slot.  The resulting tables, ctx, free list, slot metadata and live
+ * K/V equal kvc_write_prefill_kv_layers + kvc_compress (engine.py:340-358
+ * followed by compression.py:312-355) without writing the evicted rows or
+ * moving the survivors.  One sequence (args->n_seqs == 1); k/v bf16
+ * [layers][heads][L][head_dim]; args->src_pos is scratch for the call. */
+int kvc_prefill_compress(const kvc_pool *pool, const kvc_evict_args *args, const void *k,
+                         const void *v, int32_t L, void *stream);
 
 #ifdef __cplusplus
 }

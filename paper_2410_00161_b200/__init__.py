@@ -26,7 +26,7 @@ from .compression import (
     schedule_evictions,
 )
 from .metrics import MetricConfig, MetricsStore, accumulate_decode
-from .prefill import prefill_sequence, window_metrics
+from .prefill import prefill_compress_sequence, prefill_sequence, window_metrics
 
 __version__ = "0.1.0"
 
@@ -51,6 +51,7 @@ __all__ = [
     "paged_attention",
     "paged_decode",
     "per_sequence_budget",
+    "prefill_compress_sequence",
     "prefill_sequence",
     "schedule_evictions",
     "window_metrics",

@@ -72,6 +72,7 @@ class EvictArgs(ctypes.Structure):
         ("seq_rows", _p), ("budgets", _p), ("n_seqs", _i32), ("max_slots_per_head", _i64),
         ("clamped", _p), ("evict", _p), ("evicted_kvs", _p), ("freed", _p), ("moves", _p),
         ("moves_capacity", _i64), ("move_offsets", _p), ("move_counts", _p), ("totals", _p),
+        ("src_pos", _p),
     ]
 
 
@@ -97,6 +98,7 @@ _SIGS = {
     "kvc_schedule_evictions": ([_p, _p, _p], _i32),
     "kvc_execute_moves": ([_p, _p, _p], _i32),
     "kvc_compress": ([_p, _p, _p], _i32),
+    "kvc_prefill_compress": ([_p, _p, _p, _p, _i32, _p], _i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -532,6 +532,8 @@ struct MoveArgs {
   int64_t *move_off;
   int32_t *move_counts;
   int64_t *totals;
+  int32_t *src_pos;     // nullable [T][max_slots]: pre-renumbering logical of each kept position
+  int64_t src_stride;
 };
 
 // (9) per head with e > 0: mask, MoveCache pairing, copies, free, renumber.
@@ -1035,6 +1037,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
       for (int i = 0; i < 4; ++i) {
         const int pos = bl * 16 + q * 4 + i;
         const int32_t lg = lv[i];
+        if (M.src_pos && pos < Cn) M.src_pos[g * M.src_stride + pos] = (lg < 0 || lg >= n) ? -1 : lg;
         if (pos >= Cn || lg < 0 || lg >= n) continue;
         lv[i] = (int32_t)wpre[lg >> 5] + __popc(bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
       }
@@ -1449,6 +1452,7 @@ __global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int
         const int pos = bl * 16 + q * 4 + i;
         const int32_t lg = lv[i];
         if (pos >= Cn) continue;
+        if (M.src_pos) M.src_pos[g * M.src_stride + pos] = (lg < 0 || lg >= n) ? -1 : lg;
         if (lg < 0 || lg >= n) {
           if (fast) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
           continue;
@@ -1619,6 +1623,57 @@ __global__ void __launch_bounds__(256) k_copy_kv_heads(kvc_pool p, const int32_t
   }
 }
 
+// Fused prefill + compress: write every kept position's prompt row straight
+// to its final slot.  Position pos of head g (table order, after compaction)
+// holds prompt row src_pos[g][pos] (heads that evicted nothing: row pos).
+// A warp places one 16-slot block: 2 rows per instruction, 16 B per lane.
+__global__ void __launch_bounds__(256) k_place_prompt_kv(kvc_pool p, const int32_t *rows, int hp,
+                                                         const int32_t *evict, const int32_t *src_pos,
+                                                         int64_t src_stride, const uint4 *k, const uint4 *v,
+                                                         int L) {
+  const int g = blockIdx.x;
+  const int si = g / hp, hi = g % hp;
+  const int64_t hidx = (int64_t)rows[si] * hp + hi;
+  const int b = p.block_size;
+  const int vec = p.head_dim / 8;
+  const int Cn = p.ctx[hidx];
+  const int nbl = (Cn + b - 1) / b;
+  const bool moved = evict[g] > 0;
+  const int32_t *sp = src_pos + g * src_stride;
+  const uint4 *ks = k + (int64_t)hi * L * vec;  // [layer][head] = head_idx (layer-major)
+  const uint4 *vs = v + (int64_t)hi * L * vec;
+  uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
+  uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
+  const int32_t *tab = head_table(p, hidx);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nw = gridDim.y * 8;
+  for (int bl = blockIdx.y * 8 + warp; bl < nbl; bl += nw) {
+    const int64_t f0 = (int64_t)tab[bl] * b;
+    const int n = b * vec;  // chunks of the block
+    for (int c0 = 0; c0 < n; c0 += 4 * 32) {
+      uint4 tk[4], tv[4];
+      int64_t dst[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 32 + lane;
+        const int o = c / vec, pos = bl * b + o;
+        dst[u] = -1;
+        if (c < n && pos < Cn) {
+          const int src = moved ? __ldg(sp + pos) : pos;
+          if (src >= 0 && src < L) {
+            tk[u] = __ldcs(ks + (int64_t)src * vec + c % vec);
+            tv[u] = __ldcs(vs + (int64_t)src * vec + c % vec);
+            dst[u] = (f0 + o) * vec + c % vec;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (dst[u] >= 0) { kc[dst[u]] = tk[u]; vc[dst[u]] = tv[u]; }
+    }
+  }
+}
+
 __global__ void k_free_total(kvc_pool p, int64_t *totals) {
   using Red = cub::BlockReduce<int64_t, 1024>;
   __shared__ typename Red::TempStorage tmp;
@@ -1692,10 +1747,11 @@ int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, c
   return KVC_OK;
 }
 
-int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
+int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s, bool copy_kv = true) {
   const int64_t T = (int64_t)a->n_seqs * S.hp;
   if (a->totals) cudaMemsetAsync(a->totals, 0, 4 * sizeof(int64_t), s);
-  MoveArgs M{a->evict, a->evicted_kvs, a->freed, a->moves, a->move_offsets, a->move_counts, a->totals};
+  MoveArgs M{a->evict, a->evicted_kvs, a->freed, a->moves, a->move_offsets, a->move_counts, a->totals,
+             copy_kv ? nullptr : a->src_pos, S.max_slots};
   const int words = (int)((S.max_slots + 31) / 32);
   const int dyn = words * 8;  // bitmap + word prefixes
   static bool configured = false;
@@ -1718,7 +1774,7 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
   } else {
     k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
   }
-  if (pool->k_cache && T > 0) {
+  if (copy_kv && pool->k_cache && T > 0) {
     static int n_sm = 0;
     if (!n_sm) {
       int dev = 0;
@@ -1760,6 +1816,25 @@ int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *a, void *strea
   if (small_heads(S)) k_load<256><<<(int)T, 256, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0, a->clamped);
   else k_load<kThreads><<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0, a->clamped);
   return run_compact(pool, a, S, s);
+}
+
+int kvc_prefill_compress(const kvc_pool *pool, const kvc_evict_args *a, const void *k, const void *v, int32_t L,
+                         void *stream) {
+  int rc = validate(pool, a);
+  if (rc) return rc;
+  if (a->n_seqs != 1 || !a->moves || !a->src_pos || !k || !v || L < 1 || !pool->k_cache || pool->head_dim % 8 != 0 ||
+      pool->block_size != 16)
+    return KVC_ERR_INVALID;
+  Scratch sc(pool);
+  EvictState S;
+  if ((rc = setup_state(pool, a, sc, S))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = run_schedule(pool, a, S, s))) return rc;
+  if ((rc = run_compact(pool, a, S, s, /*copy_kv=*/false))) return rc;
+  k_place_prompt_kv<<<dim3((unsigned)S.hp, 4), 256, 0, s>>>(*pool, a->seq_rows, S.hp, a->evict, a->src_pos,
+                                                             S.max_slots, (const uint4 *)k, (const uint4 *)v, L);
+  KVC_CHECK_LAUNCH();
+  return KVC_OK;
 }
 
 int kvc_compress(const kvc_pool *pool, const kvc_evict_args *a, void *stream) {

@@ -152,3 +152,51 @@ def prefill_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockM
     _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
                  seq_row=tables.row(seq_id), layer=0)
     return demand
+
+
+def prefill_compress_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager,
+                              store: MetricsStore, seq_id: int, q, k, v, cfg: MetricConfig, budget_blocks: int,
+                              sync: bool = True, record_moves: bool = True, events=None):
+    """Prefill a prompt and compress it in one pass, without ever writing the
+    rows that are evicted (B200-native fusion of engine.py:340-358's prefill
+    with the on-prefill compress, compression.py:312-355).
+
+    Allocation, the window metric (K2) and the schedule/compaction (K3/K4 on
+    slot metadata) are the same kernels as prefill_sequence + compress; the
+    K/V of each surviving prompt position is then written straight to its
+    final slot.  Tables, ctx, free list, slot metadata and the K/V of every
+    live slot end up identical to prefill_sequence followed by
+    compress(..., {seq_id: budget_blocks}); freed blocks hold no prompt data.
+    Returns the CompressionSchedule (sync=True) or the EvictionPlan.
+    `events` = (start, end) CUDA events around the device work after allocation.
+    """
+    from . import compression as C
+    if cfg.mode != WINDOW:
+        raise ConfigError("mode", "the device prefill metric implements the observation window")
+    dev = cache.device
+    L = k.shape[2]
+    manager.allocate_prefill(seq_id, L)
+    kt, vt, qt = _dev_bf16(k, dev), _dev_bf16(v, dev), _dev_bf16(q, dev)
+    row = tables.row(seq_id)
+    if events:
+        events[0].record()
+    tables.ctx[row].fill_(L)  # C := L (what the scatter would set); K2 installs positions < C
+    tables.ctx_bound[row] = max(tables.ctx_bound[row], L)
+    p = pool_struct(cache=cache, tables=tables, store=store)
+    _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p, seq_row=row, layer=0)
+    plan = C._prepare(tables, {seq_id: budget_blocks}, want_moves=True, want_freed=True)
+    hp = tables.num_layers * tables.num_kv_heads
+    T = len(plan.seq_ids) * hp
+    slots = (plan.max_slots + 3) // 4 * 4
+    p = with_scratch(pool_struct(cache=cache, tables=tables, manager=manager, store=store), dev,
+                     C._scratch_bytes(plan, hp))
+    src_pos = torch.empty((max(T, 1), slots), dtype=torch.int32, device=dev)
+    a = C._args(plan)
+    a.src_pos = src_pos.data_ptr()
+    _lib.check(_lib.lib().kvc_prefill_compress(ctypes.byref(p), ctypes.byref(a), kt.data_ptr(), vt.data_ptr(), L,
+                                               _lib.stream_ptr(dev)), "prefill_compress")
+    if events:
+        events[1].record()
+    plan.executed = True
+    plan._keepalive = src_pos
+    return C._finish(tables, plan, sync, record_moves)
