@@ -44,4 +44,14 @@ for rnd in range(4):
     res.append({"round": rnd, "k2_ms": k2, "k3_ms": e4.elapsed_time(e5), "k34_ms": e2.elapsed_time(e3), "host_enqueue_ms": (t1 - t0) * 1e3,
                 "wall_ms": (t2 - t0) * 1e3, "freed": int(plan.totals[0])})
     mgr.free_sequence(rnd, store=store)
+# fused prefill + compress (K2 + K3 + K4 on metadata + survivor placement)
+for rnd in range(4, 7):
+    e0, e1 = ev(), ev()
+    torch.cuda.synchronize()
+    K.prefill_compress_sequence(cache, tables, mgr, store, rnd, q, k, v, K.MetricConfig(),
+                                K.budget_to_blocks(L // 8, l, H, b, l * H * (L // b)), sync=False, events=(e0, e1))
+    torch.cuda.synchronize()
+    _lib.DeviceContext.get(dev).raise_status()
+    res.append({"round": rnd, "fused_prefill_compress_ms": e0.elapsed_time(e1)})
+    mgr.free_sequence(rnd, store=store)
 print(json.dumps(res))
