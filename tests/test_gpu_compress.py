@@ -213,3 +213,35 @@ def test_totals_and_free_count():
     tot = plan.totals.cpu().tolist()
     assert tot[0] == want["freed_blocks"] and tot[1] == want["evicted_kvs"]
     assert tot[3] == st.free_count == rig.manager.free_count
+
+
+@pytest.mark.parametrize("name,layers,heads,L,rate", [
+    ("llama-3.1-8b full sequence", 32, 8, 32768, 8),
+    ("llama-3.1-70b 8-layer slice at 128k", 8, 8, 131072, 64),
+])
+def test_full_size_schedule_exact(name, layers, heads, L, rate):
+    """BASELINE configs at full per-sequence size: one prompt's whole cache
+    (8.4 M slots) compressed in one round, bit-exact against the oracle.
+    Schedules and move lists do not depend on head_dim, so the pool uses d=8
+    (SURVEY §8c); metrics are max-pooled (tie-heavy) fp32 like K2's."""
+    rng = np.random.default_rng(L + layers)
+    b, d = 16, 8
+    nblocks = layers * heads * (L // b) + 64
+    st = O.OracleState(nblocks, b, d, layers, heads)
+    O.alloc_prefill(st, 0, L)
+    for m in range(layers):
+        for h in range(heads):
+            st.ctx[0][m, h] = L
+            f = st.live_slots(0, m, h)
+            st.metric[f] = f32_round(O.pool_max((rng.random(L) ** 3)[None], 7)[0])
+            st.logical[f] = np.arange(L)
+            st.protected[f[-8:]] = True
+    st.keys[:] = rng.integers(-8, 8, st.keys.shape)  # exact in bf16: moved rows are checkable
+    st.values[:] = rng.integers(-8, 8, st.values.shape)
+    rig = DevRig(nblocks, b, d, layers, heads, max_seqs=2, max_blocks=L // b + 4)
+    rig.load(st)
+    E = O.budget_to_blocks(L // rate, layers, heads, b, st.block_count(0))
+    got = device_compress(rig, {0: E})
+    want = O.compress(st, {0: E})
+    assert got == want, name
+    assert_state_equal(rig, st)

@@ -107,3 +107,43 @@ def test_fused_matches_oracle():
     assert np.array_equal(dst.metric, st.metric)
     live = st.logical >= 0
     assert np.array_equal(dst.keys[live], st.keys[live]) and np.array_equal(dst.values[live], st.values[live])
+
+
+def test_fused_full_size_equals_unfused():
+    """Llama-3.1-8B shapes at full size (32 layers x 8 heads x 32k, d=128, 8x):
+    the fused path leaves the same device state as scatter + K2 + compress
+    (compared on the device; live K/V rows bit-identical)."""
+    layers, H, r, d, b, L = 32, 8, 4, 128, 16, 32768
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    q = torch.randn((layers, H * r, 8, d), generator=g, device=dev).to(torch.bfloat16)
+    k = torch.randn((layers, H, L, d), generator=g, device=dev).to(torch.bfloat16)
+    v = torch.randn((layers, H, L, d), generator=g, device=dev).to(torch.bfloat16)
+    E = K.budget_to_blocks(L // 8, layers, H, b, layers * H * (L // b))
+    rigs = []
+    for fused in (True, False):
+        nblocks = layers * H * (L // b) + 64
+        rig = DevRig(nblocks, b, d, layers, H, max_seqs=2, max_blocks=L // b + 4)
+        if fused:
+            s = K.prefill_compress_sequence(rig.cache, rig.tables, rig.manager, rig.store, 0, q, k, v,
+                                            K.MetricConfig(), E)
+        else:
+            K.prefill_sequence(rig.cache, rig.tables, rig.manager, rig.store, 0, q, k, v, K.MetricConfig())
+            s = K.compress(rig.cache, rig.tables, rig.manager, rig.store, {0: E})
+        _lib.DeviceContext.get(dev).raise_status()
+        rigs.append((rig, s.to_dict()))
+    (a, sa), (b_, sb) = rigs
+    assert sa == sb
+    assert sa["freed_blocks"] == E
+    ta, tb = a.tables, b_.tables
+    assert torch.equal(ta.nblocks, tb.nblocks) and torch.equal(ta.ctx, tb.ctx)
+    assert torch.equal(ta.tables[0], tb.tables[0])
+    assert torch.equal(a.manager.free_flag, b_.manager.free_flag)
+    for x, y in ((a.store.metrics_flat, b_.store.metrics_flat), (a.store.logical_flat, b_.store.logical_flat),
+                 (a.store.protected_flat, b_.store.protected_flat), (a.store.fresh_flat, b_.store.fresh_flat)):
+        assert torch.equal(x, y)
+    live = (a.store.logical_flat >= 0).nonzero().flatten()
+    assert live.numel() == layers * H * (L // 8)
+    assert torch.equal(a.cache.keys_flat[live], b_.cache.keys_flat[live])
+    assert torch.equal(a.cache.values_flat[live], b_.cache.values_flat[live])
