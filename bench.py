@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--metric-mode", type=int, default=2, help="decode metric: 2 L2 (reference default), 1 L1, 0 off")
     return ap.parse_args()
 
 
@@ -314,7 +315,7 @@ def decode_bench(S, args, e2e=False):
             if timed and not e2e:
                 a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-            K.paged_decode(qq[m], cache, tables, None, m, cfg, store=store, metric_mode=2, k_new=kk[m],
+            K.paged_decode(qq[m], cache, tables, None, m, cfg, store=store, metric_mode=args.metric_mode, k_new=kk[m],
                            v_new=vv[m], fresh=True, out=out[m], rows_tensor=rows_t, host_rows=rows,
                            splits=args.splits)
             if timed and not e2e:
@@ -600,7 +601,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "k_paged_decode (K1, one launch per layer)",
                      "achieved": dec["k1_gbs"], "peak": peak, "unit": "GB/s", "frac": dec["k1_gbs"] / peak,
                      "peak_source": peak_kind, "traffic": k1_traffic(),
-                     "bytes_per_launch": dec["k1_bytes_mean"], "launch_ms": dec["k1_ms_mean"]},
+                     "bytes_per_launch": dec["k1_bytes_mean"], "launch_ms": dec["k1_ms_mean"],
+                     "timing": "CUDA events around each layer's launches (stream, finish, bump) on the launching stream"},
         "eviction_step": evict,
         "clocks": dec["clocks"],
         "gpu_launches": dec["launches_per_step"] * steps,
