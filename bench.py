@@ -59,7 +59,27 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--metric-mode", type=int, default=2, help="decode metric: 2 L2 (reference default), 1 L1, 0 off")
-    return ap.parse_args()
+    ap.add_argument("--preset", default="l8b", choices=sorted(PRESETS),
+                    help="BASELINE.json config the shape flags default to (explicit flags override)")
+    args = ap.parse_args()
+    given = {a.split("=")[0].lstrip("-").replace("-", "_") for a in sys.argv[1:] if a.startswith("--")}
+    for k, v in PRESETS[args.preset]["shape"].items():
+        if k not in given:
+            setattr(args, k, v)
+    return args
+
+
+# BASELINE.json configs as shape presets (configs[1] is the default bench line)
+PRESETS = {
+    "toy": {"workload": "toy single-layer cache (BASELINE configs[0]): 4 KV heads, d=64, 2 seqs x 1k, 4x",
+            "shape": dict(layers=1, kv_heads=4, group=4, head_dim=64, context=1024, rate=4.0, batch=2)},
+    "l8b": {"workload": "llama-3.1-8b-shapes decode, 32k ctx, 8x variable-head-rate compression",
+            "shape": dict(layers=32, kv_heads=8, group=4, head_dim=128, context=32768, rate=8.0, batch=64)},
+    "m7b": {"workload": "mistral-7b-instruct-v0.2 shapes, 32k synthetic prompts, observation-window metric, 16x",
+            "shape": dict(layers=32, kv_heads=8, group=4, head_dim=128, context=32768, rate=16.0, batch=64)},
+    "l70b": {"workload": "llama-3.1-70b shapes (80 layers, 8 KV heads, GQA 8:1), 128k ctx, 64x, sequences sharded",
+             "shape": dict(layers=80, kv_heads=8, group=8, head_dim=128, context=131072, rate=64.0, batch=64)},
+}
 
 
 # ---------------------------------------------------------------------------
@@ -151,10 +171,11 @@ def build(args, dev, rank):
     per_seq_blocks = -(-keep_tokens * hp // b)
     nb_prefill = hp * (-(-L // b))
     growth = hp * (-(-(args.steps + args.warmup + 8) // b) + 2)
-    num_blocks = int(B * (per_seq_blocks * 1.25 + growth) + nb_prefill + 4096)
+    # B running sequences (at least the prefill_seqs compressed ones) + one uncompressed prompt
+    num_blocks = int(max(B, args.prefill_seqs) * (per_seq_blocks * 1.25 + growth) + nb_prefill + 4096)
     max_blocks = -(-L // b) + 8
     cache = K.UnifiedKVCache(num_blocks, b, d, device=dev)
-    tables = K.BlockTables(l, H, b, max_seqs=B + 2, max_blocks=max_blocks, device=dev)
+    tables = K.BlockTables(l, H, b, max_seqs=max(B, args.prefill_seqs) + 2, max_blocks=max_blocks, device=dev)
     manager = K.BlockManager(num_blocks, tables)
     store = K.MetricsStore(num_blocks, b, device=dev)
     cfg = K.AttentionConfig(n_q, H, d, l)
@@ -176,9 +197,9 @@ def eviction_rounds(S, args):
     out = {"k2_ms": [], "k34_ms": [], "scatter_ms": [], "freed": [], "moves": [], "evicted": []}
     for s in range(args.prefill_seqs):
         manager.allocate_prefill(s, L)
-        q = torch.randn((l, S["n_q"], 8, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-        k = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-        v = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        q = torch.randn((l, S["n_q"], 8, d), generator=S["gen"], device=dev, dtype=torch.bfloat16)
+        k = torch.randn((l, H, L, d), generator=S["gen"], device=dev, dtype=torch.bfloat16)
+        v = torch.randn((l, H, L, d), generator=S["gen"], device=dev, dtype=torch.bfloat16)
         e0, e1, e2 = ev(), ev(), ev()
         torch.cuda.synchronize()
         e0.record()
@@ -211,9 +232,9 @@ def eviction_rounds(S, args):
     out["fused_ms"] = []
     for i in range(args.prefill_seqs):
         sid = 1_000_000 + i
-        q = torch.randn((l, S["n_q"], 8, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-        k = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
-        v = torch.randn((l, H, L, d), generator=S["gen"], device=dev).to(torch.bfloat16)
+        q = torch.randn((l, S["n_q"], 8, d), generator=S["gen"], device=dev, dtype=torch.bfloat16)
+        k = torch.randn((l, H, L, d), generator=S["gen"], device=dev, dtype=torch.bfloat16)
+        v = torch.randn((l, H, L, d), generator=S["gen"], device=dev, dtype=torch.bfloat16)
         E = K.budget_to_blocks(S["keep_tokens"], l, H, b, l * H * -(-L // b))
         e0, e1 = ev(), ev()
         torch.cuda.synchronize()
@@ -484,7 +505,7 @@ def cpu_window_sample(L, H, r, d, seed=0):
 
 
 def config_dict(args, world):
-    return {"workload": "llama-3.1-8b-shapes decode, 32k ctx, 8x variable-head-rate compression",
+    return {"workload": PRESETS[args.preset]["workload"], "preset": args.preset,
             "batch_per_gpu": args.batch, "global_batch": args.batch * world, "context": args.context,
             "layers": args.layers, "kv_heads": args.kv_heads, "query_heads": args.kv_heads * args.group,
             "head_dim": args.head_dim, "block_size": 16, "compression": f"{args.rate:g}x",

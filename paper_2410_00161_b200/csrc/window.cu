@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(WinCfg<N, D, PASS, EW>::kThreads, 1)
 struct PersistParams {
   int L, Lp, H, RW, wq, start, nl, n_q;
   int tiles_per_head, cph;
+  int rs_len;       // pooling stage floats (persist_rs_len of the largest tile range)
   float scale;      // log2(e) / sqrt(d)
   int agg;          // 1 L1, 2 L2
   float2 *partial;  // [H][cph][N] (m, z) per CTA and column
@@ -409,21 +410,23 @@ constexpr int kPThreads = 64 + 32 * kPEW;
 template <int D>
 constexpr int persist_stages() { return D >= 128 ? 5 : 10; }
 
-template <int N>
-__host__ __device__ constexpr int persist_rs_len(int pool) { return ((512 / N) * kTileKeys + pool + 8 + 3) & ~3; }
+// pooling stage length (floats): a CTA's own key range + halo, 16-byte rows
+__host__ __device__ constexpr int persist_rs_len(int ntiles, int pool) {
+  return (ntiles * kTileKeys + pool + 8 + 3) & ~3;
+}
 
 template <int N, int D>
-constexpr int persist_smem(int pool) {
+constexpr int persist_smem(int pool, int ntiles) {
   return persist_stages<D>() * kTileKeys * D * 2   // K ring
          + 2 * N * D * 2                           // Q window, double-buffered over layers
-         + persist_rs_len<N>(pool) * 4              // pooling stage (own range + halo)
+         + persist_rs_len(ntiles, pool) * 4         // pooling stage (own range + halo)
          + kPEW * N * 8                            // per-warp statistics
          + 2 * N * 4 + N * 4                       // M, 1/Z, column limits
          + 512 + 1024;                             // barriers, TMEM slot, alignment
 }
 
-constexpr float kNegBig = -1e30f;
-constexpr int kMaxHalf = 7;  // pool widths up to 15 take the register path in phase C  // running-max sentinel: finite, so no inf - inf
+constexpr float kNegBig = -1e30f;  // running-max sentinel: finite, so no inf - inf
+constexpr int kMaxHalf = 7;         // pool widths up to 15 take the register path in phase C
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -498,11 +501,15 @@ __device__ __forceinline__ void epi_head_barrier(int *cnt, int target, bool lead
   named_sync(1, 32 * kPEW);
 }
 
-template <int N, int D>
+// RECOMP: a CTA's tiles of a layer exceed the TMEM slots (long prompts, e.g.
+// 128k); each layer's tiles are then streamed twice - statistics, then the
+// metric - through a rolling slot ring (K read twice from HBM).
+template <int N, int D, bool RECOMP>
 __global__ void __launch_bounds__(kPThreads, 1)
     k_window_persist(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                      const PersistParams P) {
   constexpr int kS = 512 / N;  // TMEM slots
+  constexpr int kPasses = RECOMP ? 2 : 1;
   constexpr int kStages = persist_stages<D>();
   constexpr int kAtoms = D / 64;
   constexpr int kTileBytes = kTileKeys * D * 2;
@@ -513,7 +520,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint8_t *ktiles = smem;
   uint8_t *qbuf = smem + kStages * kTileBytes;                      // [2][kQBytes]
   float *rs = reinterpret_cast<float *>(qbuf + 2 * kQBytes);        // pooling stage
-  float2 *wred = reinterpret_cast<float2 *>(rs + persist_rs_len<N>(P.pool));  // [kPEW][N]
+  float2 *wred = reinterpret_cast<float2 *>(rs + P.rs_len);         // [kPEW][N]
   float *stat_s = reinterpret_cast<float *>(wred + kPEW * N);       // M[N], 1/Z[N]
   int *lim_s = reinterpret_cast<int *>(stat_s + 2 * N);             // [N]
   uint64_t *bars = reinterpret_cast<uint64_t *>(lim_s + N);
@@ -528,7 +535,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int q_t = P.tiles_per_head / P.cph, rem_t = P.tiles_per_head % P.cph;
   const int t_lo = cidx * q_t + min(cidx, rem_t);
   const int t_hi = t_lo + q_t + (cidx < rem_t ? 1 : 0);
-  const int ntiles = t_hi - t_lo;  // >= 1, <= kS (checked on the host)
+  const int ntiles = t_hi - t_lo;  // >= 1; <= kS unless RECOMP (checked on the host)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -558,8 +565,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_expect_tx(&qfull[qb], kQBytes);
         for (int a = 0; a < kAtoms; ++a)
           tma_load_2d(qbuf + qb * kQBytes + a * N * 128, &tmQ, a * 64, (l * P.n_q) * P.wq + head * P.RW, &qfull[qb]);
-        for (int i = 0; i < ntiles; ++i) {
-          const uint32_t g = (uint32_t)(l * ntiles + i);
+        for (int gi = 0; gi < kPasses * ntiles; ++gi) {
+          const int i = gi % ntiles;
+          const uint32_t g = (uint32_t)(l * kPasses * ntiles + gi);
           const int s = g % kStages;
           if (g >= (uint32_t)kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
           mbar_expect_tx(&full[s], kTileBytes);
@@ -574,8 +582,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     for (int l = 0; l < P.nl; ++l) {
       const int qb = l & 1;
       mbar_wait(&qfull[qb], (l >> 1) & 1);
-      for (int i = 0; i < ntiles; ++i) {
-        const uint32_t g = (uint32_t)(l * ntiles + i);
+      for (int gi = 0; gi < kPasses * ntiles; ++gi) {
+        const uint32_t g = (uint32_t)(l * kPasses * ntiles + gi);
         const int s = g % kStages, slot = g % kS;
         mbar_wait(&full[s], (g / kStages) & 1);
         if (g >= (uint32_t)kS) mbar_wait(&tempty[slot], ((g / kS) - 1) & 1);
@@ -591,8 +599,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           mma_commit(&empty[s]);
           mma_commit(&tfull[slot]);
-          if (i == ntiles - 1) mma_commit(&qempty[qb]);
-          if (P.trace && i == ntiles - 1) P.trace[((int64_t)blockIdx.x * P.nl + l) * 8 + 7] = gtimer();
+          if (gi == kPasses * ntiles - 1) mma_commit(&qempty[qb]);
+          if (P.trace && gi == kPasses * ntiles - 1) P.trace[((int64_t)blockIdx.x * P.nl + l) * 8 + 7] = gtimer();
         }
         __syncwarp();
       }
@@ -611,7 +619,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (tr && et == 0) tr[0] = gtimer();
       float m[N], z[N];
       if (l < P.nl) {
-        const uint32_t gbase = (uint32_t)(l * ntiles);
+        const uint32_t gbase = (uint32_t)(l * kPasses * ntiles);
         // ---- A: online (max, sum exp2) per column, branch-free lazy rescale ----
 #pragma unroll
         for (int c = 0; c < N; ++c) { m[c] = kNegBig; z[c] = 0.f; }
@@ -638,6 +646,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 lse_step(m[h * 32 + c], z[h * 32 + c], ((vm >> c) & 1u) ? v[c] * P.scale : -INFINITY);
             }
           }
+          if (RECOMP) {  // the metric pass recomputes this tile: free the slot now
+            tc_fence_before();
+            mbar_arrive(&tempty[slot]);
+          }
         }
         // CTA partial per column: warp reduce-scatter, then fold the warps
 #pragma unroll
@@ -663,7 +675,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (tr && et == 0) tr[2] = gtimer();
 
       if (l < P.nl) {
-        const uint32_t gbase = (uint32_t)(l * ntiles);
+        const uint32_t gbase = (uint32_t)((l * kPasses + kPasses - 1) * ntiles);  // the metric pass's tiles
         // ---- B: head statistics (8 partial folds per column in parallel) ----
         {
           constexpr int kParts = 32 * kPEW / N;
@@ -698,6 +710,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int i = grp; i < ntiles; i += kPGroups) {
           const uint32_t g = gbase + i;
           const int slot = g % kS;
+          if (RECOMP) {  // recomputed tile of the metric pass
+            mbar_wait(&tfull[slot], (g / kS) & 1);
+            tc_fence_after();
+          }
           const int tile0 = (t_lo + i) * kTileKeys;
           const int j = tile0 + key_local;
           const bool fast = tile0 + kTileKeys - 1 <= P.start;
@@ -896,34 +912,42 @@ bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_r
 template <int N, int D>
 int run_persist(const kvc_pool *pool, const kvc_window_args *a, const WinParams &W, int nl, cudaStream_t s) {
   constexpr int kS = 512 / N;
-  auto fn = k_window_persist<N, D>;
   if (a->pool > 1023 || !W.bar_cnt) return KVC_ERR_UNSUPPORTED;
-  // phase C installs four contiguous slots at a time and stages the table slice in 2*kPEW*N ints
-  if (a->seq_row >= 0 && (pool->block_size % 4 != 0 || kS * kTileKeys / pool->block_size > 2 * kPEW * N))
-    return KVC_ERR_UNSUPPORTED;
-  const int smem = persist_smem<N, D>(a->pool);
-  if (smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
-  static int configured = 0, nsm = 0;
-  if (configured < smem) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static int nsm = 0;
+  if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    configured = smem;
+  }
+  // one CTA per SM: it owns all 512 TMEM columns
+  int cph = nsm / W.H;
+  if (cph > W.tiles_per_head) cph = W.tiles_per_head;
+  if (cph < 1) return KVC_ERR_UNSUPPORTED;
+  const int ntiles_max = (W.tiles_per_head + cph - 1) / cph;
+  // scores of a CTA's tiles fit in TMEM: one pass; else stream each layer twice
+  const bool recomp = ntiles_max > kS;
+  if (recomp && ntiles_max > 2 * kPEW * N * 16 / kTileKeys) return KVC_ERR_UNSUPPORTED;  // phase C table stage
+  auto fn = recomp ? k_window_persist<N, D, true> : k_window_persist<N, D, false>;
+  // phase C installs four contiguous slots at a time and stages the table slice in 2*kPEW*N ints
+  if (a->seq_row >= 0 && (pool->block_size % 4 != 0 || ntiles_max * kTileKeys / pool->block_size > 2 * kPEW * N))
+    return KVC_ERR_UNSUPPORTED;
+  const int smem = persist_smem<N, D>(a->pool, ntiles_max);
+  if (smem > 227 * 1024) return KVC_ERR_UNSUPPORTED;
+  static bool configured[2] = {false, false};
+  if (!configured[recomp]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured[recomp] = true;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPThreads, smem);
   if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
-  // one CTA per SM: it owns all 512 TMEM columns
-  int cph = nsm / W.H;
-  if (cph > W.tiles_per_head) cph = W.tiles_per_head;
-  if (cph < 1 || (W.tiles_per_head + cph - 1) / cph > kS) return KVC_ERR_UNSUPPORTED;  // scores exceed TMEM
   CUtensorMap tmK, tmQ;
   if (!make_map3(&tmK, a->k, (int64_t)nl * W.H * W.L, D, kTileKeys)) return KVC_ERR_CUDA;
   if (!make_map(&tmQ, a->q_win, (int64_t)nl * a->num_query_heads * W.wq, D, N)) return KVC_ERR_CUDA;
   PersistParams P;
   P.L = W.L; P.Lp = (W.L + 3) & ~3; P.H = W.H; P.RW = W.RW; P.wq = W.wq; P.start = W.start; P.nl = nl; P.n_q = a->num_query_heads;
   P.tiles_per_head = W.tiles_per_head; P.cph = cph;
+  P.rs_len = persist_rs_len(ntiles_max, a->pool);
   P.scale = W.scale; P.agg = W.agg;
   P.partial = W.partial; P.raw = W.raw; P.bar_cnt = W.bar_cnt;
   P.p = *pool;

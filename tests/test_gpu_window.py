@@ -80,7 +80,11 @@ def test_prefill_install_then_compress_exact():
     assert got == O.compress(st, {0: E})
 
 
-@pytest.mark.parametrize("layers,H,r,d,L", [(3, 8, 4, 128, 4100), (4, 2, 4, 64, 9000), (2, 8, 8, 128, 1500)])
+@pytest.mark.parametrize("layers,H,r,d,L", [
+    (3, 8, 4, 128, 4100), (4, 2, 4, 64, 9000), (2, 8, 8, 128, 1500),
+    (2, 8, 4, 128, 40000),   # > 16 tiles per CTA: each layer streamed twice (recompute mode)
+    (2, 8, 8, 128, 20000),   # r*w = 64 columns, > 8 tiles per CTA: recompute mode
+])
 def test_window_metric_multi_layer(layers, H, r, d, L):
     """One K2 call over several layers (the persistent kernel streams layer
     l+1 while layer l is finished) equals the oracle layer by layer."""
