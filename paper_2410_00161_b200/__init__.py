@@ -26,6 +26,7 @@ from .compression import (
     schedule_evictions,
 )
 from .metrics import MetricConfig, MetricsStore, accumulate_decode
+from .graph import DecodeStepGraph
 from .prefill import prefill_compress_sequence, prefill_sequence, window_metrics
 
 __version__ = "0.1.0"
@@ -50,6 +51,7 @@ __all__ = [
     "lookup_kv",
     "paged_attention",
     "paged_decode",
+    "DecodeStepGraph",
     "per_sequence_budget",
     "prefill_compress_sequence",
     "prefill_sequence",

@@ -35,8 +35,18 @@ constexpr int kNW = 4;           // warps per CTA
 constexpr int kThreads = kNW * 32;
 constexpr int kBlk = 16;         // tokens per KV block
 constexpr int kHP = 8;           // heads per MMA (group padded to 8)
-constexpr int kItemBlocks = 16;  // blocks per (warp) work item: 256 positions
-constexpr int kItemTok = kItemBlocks * kBlk;
+constexpr int kItemBlocks = 16;  // max blocks per (warp) work item: 256 positions
+// Blocks per work item for a launch: 16 (256 positions) unless that leaves
+// fewer than two items per resident warp (small batches), then 8/4 - more,
+// shorter split-KV items (down to 4 blocks) at the cost of more partials to merge.
+static int item_blocks_for(int64_t pairs, int max_ctx) {
+  static const int forced = getenv("KVC_K1_ITEM_BLOCKS") ? atoi(getenv("KVC_K1_ITEM_BLOCKS")) : 0;  // experiments
+  if (forced >= 1 && forced <= kItemBlocks) return forced;
+  const int64_t warps = 148 * 2 * 4;  // 2 CTAs x 4 warps per SM
+  int ib = kItemBlocks;
+  while (ib > 4 && pairs * ((max_ctx + ib * kBlk - 1) / (ib * kBlk)) < 2 * warps) ib /= 2;
+  return ib;
+}
 
 struct Params {
   kvc_pool p;
@@ -49,6 +59,8 @@ struct Params {
   int64_t rows_stride;
   int metric_mode, append_fresh, stages;
   int max_ctx_pad;  // score row length per (sequence, head)
+  int item_tok;     // positions per work item (item_blocks_for * 16)
+  int msplit;       // kernel B CTAs per (sequence, head): key slices of the metric pass
   int n_ck;         // chunks per (sequence, head) upper bound
   int n_items;
   float scale;      // log2(e)/sqrt(d)
@@ -139,9 +151,9 @@ __device__ void fetch_item(const Params &P, WItem &w, int lane) {
       const int64_t hx = head_index(p, P.rows[b_], P.layer, h_);
       const int co = p.ctx[hx];
       const int cp = co + (P.k_new ? 1 : 0);
-      const int s0 = ck * kItemTok;
+      const int s0 = ck * P.item_tok;
       if (s0 < cp && cp <= p.nblocks[hx] * kBlk) {
-        id = cand; bi = b_; head = h_; t0 = s0; t1 = min(cp, s0 + kItemTok); c_old = co; hidx = hx;
+        id = cand; bi = b_; head = h_; t0 = s0; t1 = min(cp, s0 + P.item_tok); c_old = co; hidx = hx;
         break;
       }
     }
@@ -179,7 +191,7 @@ __device__ void finish_pair(const Params &P, int bi, int head, int c_old, int la
   const int pair = bi * H + head;
   const bool append = P.k_new != nullptr;
   const int cp = c_old + (append ? 1 : 0);
-  const int nck = (cp + kItemTok - 1) / kItemTok;
+  const int nck = (cp + P.item_tok - 1) / P.item_tok;
   const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
   {
     // NumericError: non-finite query (attention.py:33-36, 108)
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       l0 += __shfl_xor_sync(0xffffffffu, l0, o);
       l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
-    const int ck = t0 / kItemTok;
+    const int ck = t0 / P.item_tok;
     float *pml = P.part_ml + ((int64_t)pair * P.n_ck + ck) * 2 * kHP;
     float *po = P.part_o + ((int64_t)pair * P.n_ck + ck) * r * D;
     if (g == 0) {
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
     if (P.fuse_finish) {
       __threadfence();  // this item's scores + partial are visible device-wide
       __syncwarp();
-      const int n_it = (c_old + (append ? 1 : 0) + kItemTok - 1) / kItemTok;
+      const int n_it = (c_old + (append ? 1 : 0) + P.item_tok - 1) / P.item_tok;
       int last = 0;
       if (lane == 0 && P.fuse_finish) last = atomicAdd(&P.pair_done[pair], 1) == n_it - 1;
       last = __shfl_sync(0xffffffffu, last, 0);
@@ -504,13 +516,14 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
 // (four slots of one block are contiguous in the pool).
 template <int R>
 __device__ __forceinline__ void metric_quads(const Params &P, const float *srow, const int32_t *tab,
-                                             const float *Ms, const float *iZ, int cp, int c_old, bool append) {
+                                             const float *Ms, const float *iZ, int cp, int c_old, bool append,
+                                             int q_lo, int q_hi) {
   const kvc_pool &p = P.p;
   float ms[R], iz[R];
 #pragma unroll
   for (int h = 0; h < R; ++h) ms[h] = Ms[h], iz[h] = iZ[h];
-  const int nq = (cp + 3) / 4;
-  for (int g = threadIdx.x; g < nq; g += blockDim.x) {
+  const int nq = min((cp + 3) / 4, q_hi);
+  for (int g = q_lo + threadIdx.x; g < nq; g += blockDim.x) {
     const int p0 = g * 4;
     float sc[4 * R];
 #pragma unroll
@@ -555,6 +568,7 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   float *Ms = sm, *iZ = sm + kHP, *fac = sm + 2 * kHP;  // fac: [n_ck][kHP]
   const kvc_pool &p = P.p;
   const int pair = blockIdx.x;
+  const int slice = blockIdx.y;  // key slice of the metric pass; slice 0 also writes the output
   const int H = p.num_kv_heads, r = P.r, n_q = H * r;
   const int bi = pair / H, head = pair % H;
   pdl_wait();
@@ -563,7 +577,7 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   const int c_old = p.ctx[hidx];
   const bool append = P.k_new != nullptr;
   const int cp = c_old + (append ? 1 : 0);
-  {
+  if (slice == 0) {
     // NumericError: non-finite query (attention.py:33-36, 108)
     const uint16_t *qg = P.q + ((int64_t)bi * n_q + head * r) * D;
     bool bad = false;
@@ -571,54 +585,71 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
     if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
   }
   if (cp < 1 || cp > p.nblocks[hidx] * kBlk) return;  // reported by k_decode_bump
-  const int nck = (cp + kItemTok - 1) / kItemTok;
+  const int nck = (cp + P.item_tok - 1) / P.item_tok;
   const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
-  if (threadIdx.x < kHP) {
-    const int h = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // head statistics: warp h folds head h's partials (lanes stride the chunks),
+  // then the merge factors fac[c][h] = exp2(m_c - M_h)
+  if (warp < kHP) {
+    const int h = warp;
     float M = -INFINITY;
-    for (int c = 0; c < nck; ++c) M = fmaxf(M, pml[c * 2 * kHP + h]);
+    for (int c = lane; c < nck; c += 32) M = fmaxf(M, __ldcg(pml + c * 2 * kHP + h));
+    M = warp_max(M);
     float Z = 0.f;
-    for (int c = 0; c < nck; ++c) {
-      const float m = pml[c * 2 * kHP + h];
+    for (int c = lane; c < nck; c += 32) {
+      const float m = __ldcg(pml + c * 2 * kHP + h);
       const float f = m == -INFINITY ? 0.f : exp2f(m - M);
       fac[c * kHP + h] = f;
-      Z += pml[c * 2 * kHP + kHP + h] * f;
+      Z += __ldcg(pml + c * 2 * kHP + kHP + h) * f;
     }
-    Ms[h] = M;
-    iZ[h] = Z > 0.f ? 1.f / Z : 0.f;
+    Z = warp_sum(Z);
+    if (lane == 0) {
+      Ms[h] = M;
+      iZ[h] = Z > 0.f ? 1.f / Z : 0.f;
+    }
   }
   __syncthreads();
-  // output
-  const float *po = P.part_o + (int64_t)pair * P.n_ck * r * D;
-  for (int e = threadIdx.x; e < r * D; e += blockDim.x) {
-    const int h = e / D;
-    float s = 0.f;
-    // independent partial loads in flight (the sum order is fixed: deterministic)
-    float acc4[4] = {0.f, 0.f, 0.f, 0.f};
-    int c = 0;
-    for (; c + 4 <= nck; c += 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc4[u] += __ldcg(po + (int64_t)(c + u) * r * D + e) * fac[(c + u) * kHP + h];
+  // output: the CTAs of the pair share the r*D outputs; with few outputs per
+  // CTA, TPO adjacent lanes split one output's chunk partials (fixed order)
+  {
+    const float *po = P.part_o + (int64_t)pair * P.n_ck * r * D;
+    const int E = r * D;
+    const int per = (E + gridDim.y - 1) / gridDim.y;
+    const int e_lo = slice * per, e_hi = min(E, e_lo + per);
+    int tpo = 1;
+    while (tpo < 32 && (e_hi - e_lo) * tpo * 2 <= (int)blockDim.x) tpo *= 2;
+    const int sub = threadIdx.x % tpo;
+    for (int e0 = e_lo + (int)threadIdx.x / tpo; e0 < e_lo + ((e_hi - e_lo + (int)blockDim.x / tpo - 1) / ((int)blockDim.x / tpo)) * ((int)blockDim.x / tpo); e0 += blockDim.x / tpo) {
+      const bool real = e0 < e_hi;
+      const int e = real ? e0 : e_lo;
+      const int h = e / D;
+      float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+      int c = sub, u = 0;
+      for (; c < nck; c += tpo, u = (u + 1) & 3) acc4[u] += __ldcg(po + (int64_t)c * E + e) * fac[c * kHP + h];
+      float s = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+      for (int o = 1; o < tpo; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (real && sub == 0) {
+        const float o = s * iZ[h];
+        const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
+        if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
+        else reinterpret_cast<__nv_bfloat16 *>(P.out)[oi] = __float2bfloat16(o);
+      }
     }
-    for (; c < nck; ++c) acc4[0] += __ldcg(po + (int64_t)c * r * D + e) * fac[c * kHP + h];
-    s = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-    const float o = s * iZ[h];
-    const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
-    if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
-    else reinterpret_cast<__nv_bfloat16 *>(P.out)[oi] = __float2bfloat16(o);
   }
   // metric / rows over all attended positions
   const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
   const int32_t *tab = head_table(p, hidx);
+  const int nq_all = (cp + 3) / 4, qper = (nq_all + gridDim.y - 1) / gridDim.y;
+  const int q_lo = slice * qper, q_hi = q_lo + qper;
   if (P.metric_mode && !P.rows_out && (r == 1 || r == 2 || r == 4 || r == 8)) {
     switch (r) {
-      case 1: metric_quads<1>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
-      case 2: metric_quads<2>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
-      case 4: metric_quads<4>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
-      default: metric_quads<8>(P, srow, tab, Ms, iZ, cp, c_old, append); break;
+      case 1: metric_quads<1>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
+      case 2: metric_quads<2>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
+      case 4: metric_quads<4>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
+      default: metric_quads<8>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
     }
   } else if (P.metric_mode || P.rows_out) {
-    for (int pos = threadIdx.x; pos < cp; pos += blockDim.x) {
+    for (int pos = q_lo * 4 + threadIdx.x; pos < min(cp, q_hi * 4); pos += blockDim.x) {
       float contrib = 0.f;
       for (int h = 0; h < r; ++h) {
         const float w = exp2f(srow[(int64_t)pos * r + h] - Ms[h]) * iZ[h];
@@ -638,7 +669,7 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
       }
     }
   }
-  if (append && !P.metric_mode && p.metric && threadIdx.x == 0) {
+  if (append && !P.metric_mode && p.metric && threadIdx.x == 0 && slice == 0) {
     const int64_t slot = (int64_t)tab[c_old / kBlk] * kBlk + c_old % kBlk;
     p.metric[slot] = 0.f;
     p.logical[slot] = c_old;
@@ -694,10 +725,11 @@ static bool pdl_off() {
   return off;
 }
 
-static void launch_pdl(void (*fn)(const Params), int grid, int threads, int smem, cudaStream_t s, const Params &P) {
+static void launch_pdl(void (*fn)(const Params), int grid, int threads, int smem, cudaStream_t s, const Params &P,
+                       int grid_y = 1) {
   const bool off = pdl_off();
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(grid, grid_y);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -760,7 +792,11 @@ int launch(Params &P, cudaStream_t s) {
   if (!P.fuse_finish) {
     const int smem_b = (2 + P.n_ck) * kHP * 4;
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
-    launch_pdl(fb, P.batch * P.p.num_kv_heads, 256, smem_b, s, P);
+    const int pairs_b = P.batch * P.p.num_kv_heads;
+    // small batches: several CTAs per (sequence, head) share the metric pass
+    int ms = 1184 / (pairs_b > 0 ? pairs_b : 1);
+    ms = ms < 1 ? 1 : ms > 8 ? 8 : ms;
+    launch_pdl(fb, pairs_b, 256, smem_b, s, P, ms);
   }
   const int pairs = P.batch * P.p.num_kv_heads;
   launch_pdl(k_decode_bump, (pairs + 255) / 256, 256, 0, s, P);
@@ -773,8 +809,9 @@ int launch(Params &P, cudaStream_t s) {
 static int64_t kvc_decode_mma_scratch(const kvc_pool *pool, int batch, int r, int max_ctx) {
   using namespace kvc_mma;
   const int64_t pairs = (int64_t)batch * pool->num_kv_heads;
-  const int64_t ctxp = ((int64_t)max_ctx + kItemTok - 1) / kItemTok * kItemTok;
-  const int64_t nck = ctxp / kItemTok;
+  const int tok = item_blocks_for(pairs, max_ctx) * kBlk;
+  const int64_t ctxp = ((int64_t)max_ctx + tok - 1) / tok * tok;
+  const int64_t nck = ctxp / tok;
   return (1 + pairs) * 4 + 256 + pairs * ctxp * r * 4 + pairs * nck * 2 * kHP * 4 + pairs * nck * r * pool->head_dim * 4 +
          4096;
 }
@@ -810,8 +847,9 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.rows_stride = a->rows_stride;
   P.metric_mode = a->metric_mode;
   P.append_fresh = a->append_fresh;
-  P.max_ctx_pad = (max_ctx + kItemTok - 1) / kItemTok * kItemTok;
-  P.n_ck = P.max_ctx_pad / kItemTok;
+  P.item_tok = item_blocks_for((int64_t)a->batch * H, max_ctx) * kBlk;
+  P.max_ctx_pad = (max_ctx + P.item_tok - 1) / P.item_tok * P.item_tok;
+  P.n_ck = P.max_ctx_pad / P.item_tok;
   P.n_items = P.n_ck * a->batch * H;
   P.scale = 1.4426950408889634f / sqrtf((float)D);
   char *base = reinterpret_cast<char *>(pool->scratch);

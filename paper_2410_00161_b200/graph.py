@@ -1,0 +1,155 @@
+"""CUDA-graph decode step: the serving engine's per-token work (engine.py:
+264-300 / 420-444) captured once and replayed.
+
+One replay = K0 decode allocation (every head whose next position opens a
+block gets one, block_manager.py:74-97) + for each layer K1 (append + paged
+GQA attention + L2/L1 metric, attention.py:92-127, metrics.py:189-211) +
+the clear of the created-this-step shield (engine.py:298).  Replaying removes
+the per-launch host work (argument structs, ctypes calls), which is what
+bounds small decode batches; the kernels are the same ones paged_decode runs.
+
+The graph bakes in device pointers and launch shapes, so it keeps its own
+workspace and work-queue, captures with `headroom` decode steps of context
+slack (the score rows are sized for it), and is recaptured automatically
+when the headroom is used up or the block tables were reallocated.
+Device-side conditions (PreemptionNeeded, AllocationOrderError, ...) land in
+the status word as usual; check them with DeviceContext.raise_status().
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .attention import AttentionConfig
+from .block_manager import BlockManager
+from .cache import BlockTables, UnifiedKVCache, pool_struct
+from .metrics import MetricsStore
+
+
+class DecodeStepGraph:
+    """Captured decode step for a fixed batch of sequences.
+
+    Inputs are written into the static buffers ``q`` (layers, B, n_q, d),
+    ``k_new`` / ``v_new`` (layers, B, H, d); ``out`` (layers, B, n_q, d)
+    receives the attention outputs.  ``step()`` replays asynchronously.
+    """
+
+    def __init__(self, cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
+                 seq_ids, cfg: AttentionConfig, metric_mode: int = 2, fresh: bool = True, headroom: int = 256,
+                 buffers: dict | None = None):
+        self.cache, self.tables, self.manager, self.store = cache, tables, manager, store
+        self.seq_ids = list(seq_ids)
+        self.cfg = cfg
+        self.metric_mode = metric_mode
+        self.fresh = fresh
+        self.headroom = headroom
+        dev = cache.device
+        self.device = dev
+        B, l = len(self.seq_ids), tables.num_layers
+        H, n_q, d = tables.num_kv_heads, cfg.num_query_heads, cfg.head_dim
+        bf = torch.bfloat16
+        b = buffers or {}
+        self.q = b.get("q", torch.zeros((l, B, n_q, d), dtype=bf, device=dev))
+        self.k_new = b.get("k_new", torch.zeros((l, B, H, d), dtype=bf, device=dev))
+        self.v_new = b.get("v_new", torch.zeros((l, B, H, d), dtype=bf, device=dev))
+        self.out = b.get("out", torch.empty((l, B, n_q, d), dtype=bf, device=dev))
+        self.rows = [tables.row(s) for s in self.seq_ids]
+        self.rows_t = torch.tensor(self.rows, dtype=torch.int32, device=dev)
+        self.alloc_order = sorted(range(B), key=lambda i: self.seq_ids[i])  # reference order: sorted(seq)
+        self.rows_sorted_t = torch.tensor([self.rows[i] for i in self.alloc_order], dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.graph = None
+        self.replays = 0
+
+    # -- capture ------------------------------------------------------------------
+
+    def _bounds(self):
+        t = self.tables
+        return max(t.ctx_bound[r] for r in self.rows)
+
+    def _capture(self) -> None:
+        t, dev = self.tables, self.device
+        B, l, H = len(self.rows), t.num_layers, t.num_kv_heads
+        self.cap_ctx = self._bounds() + self.headroom
+        t.ensure_capacity(-(-(self.cap_ctx + 1) // t.block_size) + 1)
+        self.tables_ptr = t.tables.data_ptr()
+        lib = _lib.lib()
+        # dedicated workspaces: the shared scratch may be regrown by other calls
+        p = pool_struct(cache=self.cache, tables=t, manager=self.manager, store=self.store)
+        dec_need = lib.kvc_decode_scratch_bytes(ctypes.byref(p), B, self.cfg.num_query_heads, self.cap_ctx + 1)
+        heads = B * l * H
+        alloc_need = self.manager.free_tile.numel() * 8 + heads * 8 + (1 << 16)
+        self.ws = torch.empty(max(dec_need, alloc_need) + (1 << 20), dtype=torch.uint8, device=dev)
+        self.queue = torch.zeros(1 + B * H, dtype=torch.int32, device=dev)
+        p.scratch, p.scratch_bytes = self.ws.data_ptr(), self.ws.numel()
+        args = []
+        for m in range(l):
+            a = _lib.DecodeArgs()
+            a.seq_rows = self.rows_t.data_ptr()
+            a.batch = B
+            a.layer = m
+            a.num_query_heads = self.cfg.num_query_heads
+            a.q = self.q[m].data_ptr()
+            a.k_new = self.k_new[m].data_ptr()
+            a.v_new = self.v_new[m].data_ptr()
+            a.out = self.out[m].data_ptr()
+            a.out_f32 = 0
+            a.rows_out = None
+            a.rows_stride = 0
+            a.metric_mode = self.metric_mode
+            a.append_fresh = int(self.fresh)
+            a.max_ctx = self.cap_ctx + 1
+            a.splits = 0
+            a.queue = self.queue.data_ptr()
+            args.append(a)
+        self._keep = (p, args)
+
+        def body(stream):
+            _lib.check(lib.kvc_alloc_decode(ctypes.byref(p), self.rows_sorted_t.data_ptr(), B, self.counts.data_ptr(),
+                                            stream), "alloc_decode")
+            for a in args:
+                _lib.check(lib.kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), stream), "paged_decode")
+            _lib.check(lib.kvc_clear_fresh(ctypes.byref(p), self.rows_t.data_ptr(), B, stream), "clear_fresh")
+
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                body(s.cuda_stream)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        self.captured_at = self._bounds()
+
+    def _valid(self) -> bool:
+        return (self.graph is not None and self.tables.tables.data_ptr() == self.tables_ptr
+                and self._bounds() + 1 <= self.cap_ctx)
+
+    def step(self) -> torch.Tensor:
+        """One decode step for the batch: allocation, every layer, fresh clear.
+        Asynchronous; returns the output buffer.  The first call runs the step
+        eagerly (configuring every kernel outside a capture) and captures the
+        graph for the following calls."""
+        if self.graph is None:
+            self._eager_step()
+            self._capture()
+            return self.out
+        if not self._valid():
+            self._capture()
+        self.graph.replay()
+        for r in self.rows:
+            self.tables.ctx_bound[r] += 1
+        self.replays += 1
+        return self.out
+
+    def _eager_step(self) -> None:
+        """The same step through paged_decode (kernel attributes, tensor maps)."""
+        from .attention import paged_decode
+        self.manager.allocate_decode_step(self.seq_ids, sync=False)
+        for m in range(self.tables.num_layers):
+            paged_decode(self.q[m], self.cache, self.tables, None, m, self.cfg, store=self.store,
+                         metric_mode=self.metric_mode, k_new=self.k_new[m], v_new=self.v_new[m], fresh=self.fresh,
+                         out=self.out[m], rows_tensor=self.rows_t, host_rows=self.rows)
+        self.store.clear_fresh(self.tables, self.seq_ids)
