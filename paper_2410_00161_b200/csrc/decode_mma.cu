@@ -22,6 +22,9 @@
 // grid-wide synchronisation.
 #include <cuda.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -71,6 +74,7 @@ struct Params {
   float *scores;    // [pairs][max_ctx_pad][r]
   float *part_ml;   // [pairs][n_ck][2][kHP]
   float *part_o;    // [pairs][n_ck][r][D]
+  unsigned long long *trace;  // debug (KVC_K1_TRACE): [grid*warps][2] start/end globaltimer
 };
 
 // Programmatic dependent launch: the finish and bump kernels are launched
@@ -312,6 +316,11 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int H = p.num_kv_heads, r = P.r, n_q = H * r;
+  if (P.trace && lane == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    P.trace[(blockIdx.x * kNW + warp) * 2] = t0;
+  }
   const bool append = P.k_new != nullptr;
   uint8_t *my_ring = smem + warp * stages * kStageBytes;
   uint64_t *my_bars = reinterpret_cast<uint64_t *>(smem + kNW * stages * kStageBytes) + warp * stages;
@@ -508,6 +517,11 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
     else if (lane == 0) wit[fin].id = -1;
     __syncwarp();
     if (lane == 0) try_issue();
+  }
+  if (P.trace && lane == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+    P.trace[(blockIdx.x * kNW + warp) * 2 + 1] = t1;
   }
 }
 
@@ -789,6 +803,24 @@ int launch(Params &P, cudaStream_t s) {
     cfg.numAttrs = pdl_off() ? 0 : 1;
     cudaLaunchKernelEx(&cfg, fa, tmK, tmV, P);
   }
+  if (P.trace) {
+    // debug: spread of the warps' end times in this launch (synchronises)
+    const int nw = grid * kNW;
+    unsigned long long *h = (unsigned long long *)malloc((size_t)nw * 16);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, P.trace, (size_t)nw * 16, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, e_min = ~0ull, e_max = 0;
+    for (int i = 0; i < nw; ++i) {
+      t0 = h[2 * i] < t0 ? h[2 * i] : t0;
+      e_min = h[2 * i + 1] < e_min ? h[2 * i + 1] : e_min;
+      e_max = h[2 * i + 1] > e_max ? h[2 * i + 1] : e_max;
+    }
+    double e_mean = 0;
+    for (int i = 0; i < nw; ++i) e_mean += (double)(h[2 * i + 1] - t0) / nw;
+    fprintf(stderr, "[k1 trace] items %d warps %d: warp end min %.1f mean %.1f max %.1f us after first start\n", P.n_items,
+            nw, (e_min - t0) / 1e3, e_mean / 1e3, (e_max - t0) / 1e3);
+    free(h);
+  }
   if (!P.fuse_finish) {
     const int smem_b = (2 + P.n_ck) * kHP * 4;
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
@@ -864,6 +896,16 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.part_ml = reinterpret_cast<float *>(base + off);
   off += (int64_t)a->batch * H * P.n_ck * 2 * kHP * 4;
   P.part_o = reinterpret_cast<float *>(base + off);
+  P.trace = nullptr;
+  {
+    static int calls = 0;
+    static unsigned long long *tbuf = nullptr;
+    static const bool tr = getenv("KVC_K1_TRACE") != nullptr;
+    if (tr && ++calls % 97 == 0) {  // every 97th launch (not under graph capture)
+      if (!tbuf) cudaMalloc(&tbuf, 148 * 4 * kNW * 16);
+      P.trace = tbuf;
+    }
+  }
   switch (D) {
     case 64: return launch<64>(P, s);
     case 128: return launch<128>(P, s);
