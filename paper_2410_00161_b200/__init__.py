@@ -26,6 +26,7 @@ from .compression import (
     schedule_evictions,
 )
 from .metrics import MetricConfig, MetricsStore, accumulate_decode
+from .engine import POLICY_PRESETS, CompressionPolicy, Engine, StepRecord, select_compression_batch
 from .graph import DecodeStepGraph
 from .prefill import prefill_compress_sequence, prefill_sequence, window_metrics
 
@@ -52,6 +53,11 @@ __all__ = [
     "paged_attention",
     "paged_decode",
     "DecodeStepGraph",
+    "Engine",
+    "CompressionPolicy",
+    "POLICY_PRESETS",
+    "StepRecord",
+    "select_compression_batch",
     "per_sequence_budget",
     "prefill_compress_sequence",
     "prefill_sequence",
