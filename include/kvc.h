@@ -26,6 +26,7 @@
  *                           fused)                            attention.py:92-127,
  *                                                             metrics.py:189-211
  *   kvc_accumulate_rows     accumulate_decode                 metrics.py:189-211
+ *   kvc_full_metric         gqa_attention -> full_metrics     metrics.py:92-109
  *   kvc_window_metric       gqa_attention -> window_metrics -> write_prompt_pass
  *                                                             attention.py:62-89,
  *                                                             metrics.py:68-89,160-175
@@ -227,6 +228,23 @@ typedef struct kvc_window_args {
 } kvc_window_args;
 
 int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *args, void *stream);
+
+/* ---- f3: KVC-full metric (prefill) --------------------------------------- */
+
+typedef struct kvc_full_args {
+  int32_t num_query_heads;
+  int32_t L;                /* prompt length */
+  const void *q;            /* bf16 [n_q][L][head_dim] (all prompt queries) */
+  const void *k;            /* bf16 [heads][L][head_dim] */
+  int32_t excluded;         /* v: key j aggregates queries i >= j + v */
+  int32_t aggregation;      /* 1 L1, 2 L2 */
+  float *metrics_out;       /* f32 [heads][L] */
+} kvc_full_args;
+
+/* full_metrics (metrics.py:92-109) over gqa_attention's causal softmax
+ * (attention.py:62-89) for one layer, on tcgen05: row statistics, then
+ * column sums over rows i >= j + v.  Install with kvc_write_prompt_pass. */
+int kvc_full_metric(const kvc_pool *pool, const kvc_full_args *args, void *stream);
 
 /* ---- K3 + K4: eviction schedule and compaction --------------------------- */
 

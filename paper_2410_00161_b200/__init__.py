@@ -28,7 +28,7 @@ from .compression import (
 from .metrics import MetricConfig, MetricsStore, accumulate_decode
 from .engine import POLICY_PRESETS, CompressionPolicy, Engine, StepRecord, select_compression_batch
 from .graph import DecodeStepGraph
-from .prefill import prefill_compress_sequence, prefill_sequence, window_metrics
+from .prefill import full_metrics, prefill_compress_sequence, prefill_sequence, window_metrics
 
 __version__ = "0.1.0"
 
@@ -61,6 +61,7 @@ __all__ = [
     "per_sequence_budget",
     "prefill_compress_sequence",
     "prefill_sequence",
+    "full_metrics",
     "schedule_evictions",
     "window_metrics",
 ]

@@ -67,6 +67,13 @@ class WindowArgs(ctypes.Structure):
     ]
 
 
+class FullArgs(ctypes.Structure):
+    _fields_ = [
+        ("num_query_heads", _i32), ("L", _i32), ("q", _p), ("k", _p), ("excluded", _i32), ("aggregation", _i32),
+        ("metrics_out", _p),
+    ]
+
+
 class EvictArgs(ctypes.Structure):
     _fields_ = [
         ("seq_rows", _p), ("budgets", _p), ("n_seqs", _i32), ("max_slots_per_head", _i64),
@@ -98,6 +105,7 @@ _SIGS = {
     "kvc_schedule_evictions": ([_p, _p, _p], _i32),
     "kvc_execute_moves": ([_p, _p, _p], _i32),
     "kvc_compress": ([_p, _p, _p], _i32),
+    "kvc_full_metric": ([_p, _p, _p], _i32),
     "kvc_prefill_compress": ([_p, _p, _p, _p, _i32, _p], _i32),
 }
 

@@ -22,7 +22,7 @@ from .attention import AttentionConfig
 from .block_manager import BlockManager
 from .cache import BlockTables, UnifiedKVCache, pool_struct, with_scratch
 from .errors import ConfigError
-from .metrics import WINDOW, MetricConfig, MetricsStore
+from .metrics import FULL, WINDOW, MetricConfig, MetricsStore
 
 
 def _dev_bf16(x, dev) -> torch.Tensor:
@@ -94,6 +94,51 @@ def window_metrics(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
     return out, protected
 
 
+def _full_call(q, k, cfg: MetricConfig, num_kv_heads: int, dev, out) -> None:
+    """KVC-full metric of one layer on tcgen05: q (n_q, L, d), k (H, L, d) bf16
+    -> out (H, L) f32 (csrc/fullmetric.cu)."""
+    n_q, L, d = q.shape
+    a = _lib.FullArgs()
+    a.num_query_heads = n_q
+    a.L = L
+    a.q = q.data_ptr()
+    a.k = k.data_ptr()
+    a.excluded = cfg.excluded
+    a.aggregation = cfg.metric_mode
+    a.metrics_out = out.data_ptr()
+    p = _lib.KvcPool()
+    p.status = _lib.DeviceContext.get(dev).status.data_ptr()
+    p.num_kv_heads = num_kv_heads
+    p.head_dim = d
+    nt = -(-L // 128)
+    with_scratch(p, dev, n_q * nt * 128 * 4 + (1 << 16))
+    _lib.check(_lib.lib().kvc_full_metric(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)), "full_metric")
+
+
+def full_metrics(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
+    """KVC-full metrics of one layer (metrics.py:92-109): q (n_q, L, d) all
+    prompt queries, k (num_kv_heads, L, d).  Returns (metrics (H, L) fp32,
+    protected (L,) all False) like prompt_metrics in full mode."""
+    dev = _lib.require_cuda(device if device is not None else (q.device if torch.is_tensor(q) and q.is_cuda else None))
+    qt, kt = _dev_bf16(q, dev), _dev_bf16(k, dev)
+    out = torch.empty((num_kv_heads, kt.shape[1]), dtype=torch.float32, device=dev)
+    _full_call(qt, kt, cfg, num_kv_heads, dev, out)
+    return out, torch.zeros(kt.shape[1], dtype=torch.bool, device=dev)
+
+
+def _install_full(cache, tables, store, seq_id, qt, kt, cfg: MetricConfig) -> None:
+    """Full-mode prefill metric: per layer K_full -> write_prompt_pass (no protection)."""
+    dev = cache.device
+    nl, H, L = kt.shape[0], kt.shape[1], kt.shape[2]
+    buf = torch.empty((H, L), dtype=torch.float32, device=dev)
+    row = tables.row(seq_id)
+    p = pool_struct(cache=cache, tables=tables, store=store)
+    for layer in range(nl):
+        _full_call(qt[layer], kt[layer], cfg, H, dev, buf)
+        _lib.check(_lib.lib().kvc_write_prompt_pass(ctypes.byref(p), row, layer, buf.data_ptr(), L, None, L,
+                                                    _lib.stream_ptr(dev)), "write_prompt_pass")
+
+
 def write_prefill_kv(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, layer: int, k, v) -> None:
     """Scatter one layer's prompt K/V (heads, L, d) into the head tables; C := L."""
     dev = cache.device
@@ -135,19 +180,23 @@ def prefill_layer(cache: UnifiedKVCache, tables: BlockTables, store: MetricsStor
 
 def prefill_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
                      seq_id: int, q, k, v, cfg: MetricConfig, attn: AttentionConfig | None = None) -> int:
-    """Allocate + write + score a prompt: q (l, n_q, L or w, d), k/v (l, H, L, d).
+    """Allocate + write + score a prompt: q (l, n_q, L or w, d) (all L rows
+    for the full metric), k/v (l, H, L, d).
 
     Raises PreemptionNeeded (nothing allocated) when the pool is short.
     Returns the number of blocks allocated.  Asynchronous after allocation:
     all layers' scatters, then one K2 call covering every layer.
     """
-    if cfg.mode != WINDOW:
-        raise ConfigError("mode", "the device prefill metric implements the observation window")
     dev = cache.device
     L = k.shape[2]
+    if cfg.mode == FULL and q.shape[2] != L:
+        raise ValueError("the full metric needs every prompt query: q (l, n_q, L, d)")
     demand = manager.allocate_prefill(seq_id, L)
     kt, vt, qt = _dev_bf16(k, dev), _dev_bf16(v, dev), _dev_bf16(q, dev)
     write_prefill_kv_layers(cache, tables, seq_id, kt, vt)
+    if cfg.mode == FULL:
+        _install_full(cache, tables, store, seq_id, qt, kt, cfg)
+        return demand
     p = pool_struct(cache=cache, tables=tables, store=store)
     _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
                  seq_row=tables.row(seq_id), layer=0)
