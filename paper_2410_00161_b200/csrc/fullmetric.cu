@@ -27,7 +27,10 @@ using namespace kvc;
 namespace {
 
 constexpr int kT = 128;        // rows / keys per tile
-constexpr int kFThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue (one TMEM lane quadrant each)
+// warp 0 TMA, warp 1 MMA, 8 epilogue warps: two per TMEM lane quadrant, each
+// taking half of a tile's 128 columns (more exp2 in flight per SM)
+constexpr int kEpiW = 8;
+constexpr int kFThreads = 64 + 32 * kEpiW;
 
 template <int D>
 constexpr int full_stages() { return D >= 128 ? 4 : 8; }
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * kEpiW); }
     mbar_init(qfull, 1);
     fence_barrier_init();
   }
@@ -128,34 +131,48 @@ __global__ void __launch_bounds__(kFThreads, 1)
       __syncwarp();
     }
   } else {
-    const int quad = warp & 3;
+    const int quad = warp & 3, half = (warp - 2) / 4;
     const int row = quad * 32 + lane;
     const int i = qt * kT + row;  // query position
-    float m = -1e30f, z = 0.f;
+    // four independent (max, sum) chains per thread (columns e % 4)
+    float m[4] = {-1e30f, -1e30f, -1e30f, -1e30f}, z[4] = {0.f, 0.f, 0.f, 0.f};
     for (int t = 0; t < ntk; ++t) {
       const int acc = t & 1;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
       const bool diag = t == qt;
 #pragma unroll
-      for (int c = 0; c < kT / 32; ++c) {
+      for (int c = 0; c < kT / 64; ++c) {
+        const int col0 = half * (kT / 2) + c * 32;
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * kT + c * 32, v);
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * kT + col0, v);
         if (!diag) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) lse_elem(m, z, v[e] * P.scale);
+          for (int e = 0; e < 32; ++e) lse_elem(m[e & 3], z[e & 3], v[e] * P.scale);
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const int j = t * kT + c * 32 + e;
-            lse_elem(m, z, (j <= i) ? v[e] * P.scale : -INFINITY);
+            const int j = t * kT + col0 + e;
+            lse_elem(m[e & 3], z[e & 3], (j <= i) ? v[e] * P.scale : -INFINITY);
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
-    if (i < P.L) P.cst[(int64_t)h * P.nt * kT + i] = m + __log2f(z);
+    // merge the chains, then the two column halves of the row through smem
+    float mm = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+    float zz = z[0] * ex2_approx(m[0] - mm) + z[1] * ex2_approx(m[1] - mm) + z[2] * ex2_approx(m[2] - mm) +
+               z[3] * ex2_approx(m[3] - mm);
+    float2 *xs = reinterpret_cast<float2 *>(ring);  // the ring is idle now (all MMAs consumed)
+    if (half == 1) xs[row] = make_float2(mm, zz);
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiW) : "memory");
+    if (half == 0) {
+      const float2 o = xs[row];
+      const float mn = fmaxf(mm, o.x);
+      zz = zz * ex2_approx(mm - mn) + o.y * ex2_approx(o.x - mn);
+      if (i < P.L) P.cst[(int64_t)h * P.nt * kT + i] = mn + __log2f(zz);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -191,8 +208,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
   if (threadIdx.x == 0) {
     // empty[s]: all 128 epilogue threads have read the stage's c_i (the MMA's
     // read of its Q tile completed before tfull)
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 128); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 32 * kEpiW); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * kEpiW); }
     mbar_init(kfull, 1);
     fence_barrier_init();
   }
@@ -237,12 +254,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
       }
     }
   } else {
-    const int quad = warp & 3;
+    const int quad = warp & 3, half = (warp - 2) / 4;
     const int key = quad * 32 + lane;
     const int j = j0 + key;
     const float sc = P.agg == 2 ? 2.f * P.scale : P.scale;
     const float cm = P.agg == 2 ? 2.f : 1.f;
-    float acc_sum = 0.f;
+    float acc_sum = 0.f, acc_b = 0.f;  // two FADD chains
     for (int w = 0; w < nwork; ++w) {
       const int s = w % kStages, acc = w & 1;
       const int qt = qt0 + w % nq_t;
@@ -252,17 +269,21 @@ __global__ void __launch_bounds__(kFThreads, 1)
       // every row of the tile is >= j + v and < L: no masks
       const bool inner = qt * kT >= j0 + kT - 1 + P.v && qt * kT + kT <= P.L;
 #pragma unroll
-      for (int c = 0; c < kT / 32; ++c) {
+      for (int c = 0; c < kT / 64; ++c) {
+        const int col0 = half * (kT / 2) + c * 32;
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * kT + c * 32, v);
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * kT + col0, v);
         if (inner) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) acc_sum += ex2_approx(fmaf(v[e], sc, -cm * cs[c * 32 + e]));
+          for (int e = 0; e < 32; e += 2) {
+            acc_sum += ex2_approx(fmaf(v[e], sc, -cm * cs[col0 + e]));
+            acc_b += ex2_approx(fmaf(v[e + 1], sc, -cm * cs[col0 + e + 1]));
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const int i = qt * kT + c * 32 + e;
-            const float f = ex2_approx(fmaf(v[e], sc, -cm * cs[c * 32 + e]));
+            const int i = qt * kT + col0 + e;
+            const float f = ex2_approx(fmaf(v[e], sc, -cm * cs[col0 + e]));
             acc_sum += (i >= j + P.v && i < P.L) ? f : 0.f;
           }
         }
@@ -271,7 +292,12 @@ __global__ void __launch_bounds__(kFThreads, 1)
       mbar_arrive(&tempty[acc]);
       mbar_arrive(&empty[s]);
     }
-    if (j < P.L) P.out[(int64_t)hk * P.L + j] = acc_sum;
+    // the two halves of the key's query rows: sum through smem (ring idle now)
+    float *xs = reinterpret_cast<float *>(kbuf);
+    acc_sum += acc_b;
+    if (half == 1) xs[key] = acc_sum;
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiW) : "memory");
+    if (half == 0 && j < P.L) P.out[(int64_t)hk * P.L + j] = acc_sum + xs[key];
   }
   tc_fence_before();
   __syncthreads();
