@@ -40,7 +40,7 @@ struct FullParams {
   int nt;               // tiles along L
   float scale;          // log2(e) / sqrt(d)
   int agg;              // 1 L1, 2 L2
-  float *cst;           // [n_q][L] per-row log2 normalisers (F1 out, F2 in)
+  float *cst;           // [n_q][nt*128] per-row log2 normalisers x f's power (F1 out, F2 in)
   float *out;           // [H][L] metrics
 };
 
@@ -147,8 +147,19 @@ __global__ void __launch_bounds__(kFThreads, 1)
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + acc * kT + col0, v);
         if (!diag) {
+          // chunk max first (one FMNMX per score), one rescale per chunk and
+          // chain, then exp2 + add per score: ~4 instructions per score
+          float cmax[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
-          for (int e = 0; e < 32; ++e) lse_elem(m[e & 3], z[e & 3], v[e] * P.scale);
+          for (int e = 4; e < 32; ++e) cmax[e & 3] = fmaxf(cmax[e & 3], v[e]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float mn = fmaxf(m[q], cmax[q] * P.scale);
+            z[q] *= ex2_approx(m[q] - mn);
+            m[q] = mn;
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) z[e & 3] += ex2_approx(fmaf(v[e], P.scale, -m[e & 3]));
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
@@ -171,7 +182,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
       const float2 o = xs[row];
       const float mn = fmaxf(mm, o.x);
       zz = zz * ex2_approx(mm - mn) + o.y * ex2_approx(o.x - mn);
-      if (i < P.L) P.cst[(int64_t)h * P.nt * kT + i] = mn + __log2f(zz);
+      // stored pre-multiplied by f's power (2 for L2): F2 computes exp2(pow*s - cst)
+      if (i < P.L) P.cst[(int64_t)h * P.nt * kT + i] = (P.agg == 2 ? 2.f : 1.f) * (mn + __log2f(zz));
     }
   }
   tc_fence_before();
@@ -258,7 +270,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
     const int key = quad * 32 + lane;
     const int j = j0 + key;
     const float sc = P.agg == 2 ? 2.f * P.scale : P.scale;
-    const float cm = P.agg == 2 ? 2.f : 1.f;
     float acc_sum = 0.f, acc_b = 0.f;  // two FADD chains
     for (int w = 0; w < nwork; ++w) {
       const int s = w % kStages, acc = w & 1;
@@ -276,14 +287,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
         if (inner) {
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            acc_sum += ex2_approx(fmaf(v[e], sc, -cm * cs[col0 + e]));
-            acc_b += ex2_approx(fmaf(v[e + 1], sc, -cm * cs[col0 + e + 1]));
+            acc_sum += ex2_approx(fmaf(v[e], sc, -cs[col0 + e]));
+            acc_b += ex2_approx(fmaf(v[e + 1], sc, -cs[col0 + e + 1]));
           }
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const int i = qt * kT + col0 + e;
-            const float f = ex2_approx(fmaf(v[e], sc, -cm * cs[col0 + e]));
+            const float f = ex2_approx(fmaf(v[e], sc, -cs[col0 + e]));
             acc_sum += (i >= j + P.v && i < P.L) ? f : 0.f;
           }
         }
