@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--metric-mode", type=int, default=2, help="decode metric: 2 L2 (reference default), 1 L1, 0 off")
+    ap.add_argument("--no-metric-overlap", action="store_true",
+                    help="graph step: accumulate the metric in the finish kernel instead of a side branch")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the decode step layer by layer instead of replaying its CUDA graph")
     ap.add_argument("--preset", default="l8b", choices=sorted(PRESETS),
@@ -328,7 +330,8 @@ def decode_bench(S, args, e2e=False):
     graph = None
     if not args.no_graph:
         graph = K.DecodeStepGraph(cache, tables, manager, store, seqs, cfg, metric_mode=args.metric_mode,
-                                  headroom=max(64, args.steps + args.warmup + 8))
+                                  headroom=max(64, args.steps + args.warmup + 8),
+                                  metric_overlap=not args.no_metric_overlap)
 
     def one_step(i, timed):
         sel = i % n_sets

@@ -184,6 +184,11 @@ typedef struct kvc_decode_args {
                                that is zero on entry; the call leaves it zero, so
                                the caller allocates it once and skips a memset
                                per call.  NULL: the call zeroes a scratch copy. */
+  void *metric_stream;      /* NULL, or a cudaStream_t: the metric accumulation
+                               (metric_mode, no rows_out) runs there, forked
+                               after this call's attention; the caller joins it
+                               and must not reuse this call's scratch before
+                               (DecodeStepGraph double-buffers). */
 } kvc_decode_args;
 
 int kvc_paged_decode(const kvc_pool *pool, const kvc_decode_args *args, void *stream);

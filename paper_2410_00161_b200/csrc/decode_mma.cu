@@ -68,8 +68,9 @@ struct Params {
   int n_items;
   float scale;      // log2(e)/sqrt(d)
   int *counter;     // work queue head (reset by k_decode_bump for the next call)
-  int *pair_done;   // [pairs] items completed per (sequence, head)
-  int fuse_finish;  // 1: the warp completing a pair's last item finishes it (no kernel B)
+  int *pair_done;   // [pairs] reserved per-pair counters (kept zero by k_decode_bump)
+  int metric_split; // 1: kernel B writes the output only; k_decode_metric (side stream) accumulates
+  void *metric_stream;
   int counter_ready;
   float *scores;    // [pairs][max_ctx_pad][r]
   float *part_ml;   // [pairs][n_ck][2][kHP]
@@ -180,104 +181,6 @@ __device__ void fetch_item(const Params &P, WItem &w, int lane) {
     w.id = id; w.bi = bi; w.head = head; w.t0 = t0; w.t1 = t1; w.c_old = c_old; w.nblk = nblk; w.hidx = hidx;
   }
   __syncwarp();
-}
-
-// One warp finishes a (sequence, KV head) once all its items are in:
-// merge the split partials (log-sum-exp), write the output and fold
-// f(exp2(s - M) / Z) into every attended slot's metric (reference:
-// attention.py:92-127 output, metrics.py:189-211 accumulation; the appended
-// slot gets metric/logical/fresh, metrics.py:153-158).  ctx is bumped later
-// by k_decode_bump (other warps may still be reading it).
-template <int D>
-__device__ void finish_pair(const Params &P, int bi, int head, int c_old, int lane) {
-  const kvc_pool &p = P.p;
-  const int H = p.num_kv_heads, r = P.r, n_q = H * r;
-  const int pair = bi * H + head;
-  const bool append = P.k_new != nullptr;
-  const int cp = c_old + (append ? 1 : 0);
-  const int nck = (cp + P.item_tok - 1) / P.item_tok;
-  const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
-  {
-    // NumericError: non-finite query (attention.py:33-36, 108)
-    const uint16_t *qg = P.q + ((int64_t)bi * n_q + head * r) * D;
-    bool bad = false;
-    for (int e = lane; e < r * D; e += 32) bad |= !isfinite(bf16_bits_to_f32(qg[e]));
-    if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)pair, 0);
-  }
-  // lane h < kHP: head statistics
-  float M = -INFINITY, Z = 0.f;
-  if (lane < kHP) {
-    for (int c = 0; c < nck; ++c) M = fmaxf(M, __ldcg(pml + c * 2 * kHP + lane));
-    for (int c = 0; c < nck; ++c) {
-      const float m = __ldcg(pml + c * 2 * kHP + lane);
-      if (m != -INFINITY) Z += __ldcg(pml + c * 2 * kHP + kHP + lane) * exp2f(m - M);
-    }
-  }
-  float Mh[kHP], iZ[kHP];
-#pragma unroll
-  for (int h = 0; h < kHP; ++h) {
-    Mh[h] = __shfl_sync(0xffffffffu, M, h);
-    const float z = __shfl_sync(0xffffffffu, Z, h);
-    iZ[h] = z > 0.f ? 1.f / z : 0.f;
-  }
-  // output (r x D)
-  const float *po = P.part_o + (int64_t)pair * P.n_ck * r * D;
-  for (int e = lane; e < r * D; e += 32) {
-    const int h = e / D;
-    float mh = Mh[0];
-#pragma unroll
-    for (int k = 1; k < kHP; ++k) mh = h == k ? Mh[k] : mh;
-    float izh = iZ[0];
-#pragma unroll
-    for (int k = 1; k < kHP; ++k) izh = h == k ? iZ[k] : izh;
-    float s = 0.f;
-    for (int c = 0; c < nck; ++c) {
-      const float m = __ldcg(pml + c * 2 * kHP + h);
-      if (m != -INFINITY) s += __ldcg(po + (int64_t)c * r * D + e) * exp2f(m - mh);
-    }
-    const float o = s * izh;
-    const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
-    if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
-    else reinterpret_cast<__nv_bfloat16 *>(P.out)[oi] = __float2bfloat16(o);
-  }
-  // metric / rows over every attended position
-  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
-  const int32_t *tab = head_table(p, hidx);
-  const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
-  if (P.metric_mode || P.rows_out) {
-    for (int pos = lane; pos < cp; pos += 32) {
-      float contrib = 0.f;
-      for (int h = 0; h < r; ++h) {
-        float mh = Mh[0], izh = iZ[0];
-#pragma unroll
-        for (int k = 1; k < kHP; ++k) {
-          mh = h == k ? Mh[k] : mh;
-          izh = h == k ? iZ[k] : izh;
-        }
-        const float w = exp2f(__ldcg(srow + (int64_t)pos * r + h) - mh) * izh;
-        contrib += P.metric_mode == 2 ? w * w : w;
-        if (P.rows_out) P.rows_out[(((int64_t)bi * H + head) * r + h) * P.rows_stride + pos] = w;
-      }
-      if (P.metric_mode) {
-        const int64_t slot = (int64_t)tab[pos / kBlk] * kBlk + pos % kBlk;
-        if (append && pos == c_old) {
-          p.metric[slot] = contrib;
-          p.logical[slot] = c_old;
-          p.protected_[slot] = 0;
-          p.fresh[slot] = P.append_fresh ? 1 : 0;
-        } else {
-          p.metric[slot] += contrib;
-        }
-      }
-    }
-  }
-  if (append && !P.metric_mode && p.metric && lane == 0) {
-    const int64_t slot = (int64_t)tab[c_old / kBlk] * kBlk + c_old % kBlk;
-    p.metric[slot] = 0.f;
-    p.logical[slot] = c_old;
-    p.protected_[slot] = 0;
-    p.fresh[slot] = P.append_fresh ? 1 : 0;
-  }
 }
 
 // After kernel A: status checks for heads that produced no item, C += 1 for
@@ -494,19 +397,6 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       }
     }
     (void)item_id;
-    // last item of this (sequence, head)?  then this warp finishes the pair
-    if (P.fuse_finish) {
-      __threadfence();  // this item's scores + partial are visible device-wide
-      __syncwarp();
-      const int n_it = (c_old + (append ? 1 : 0) + P.item_tok - 1) / P.item_tok;
-      int last = 0;
-      if (lane == 0 && P.fuse_finish) last = atomicAdd(&P.pair_done[pair], 1) == n_it - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        __threadfence();
-        finish_pair<D>(P, bi, head, c_old, lane);
-      }
-    }
     // advance: the fetched-ahead item becomes current; refill the other slot
     const int fin = cur;
     cur ^= 1;
@@ -650,6 +540,7 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
       }
     }
   }
+  if (P.metric_split) return;  // k_decode_metric accumulates on the side stream
   // metric / rows over all attended positions
   const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
   const int32_t *tab = head_table(p, hidx);
@@ -689,6 +580,54 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
     p.logical[slot] = c_old;
     p.protected_[slot] = 0;
     p.fresh[slot] = P.append_fresh ? 1 : 0;
+  }
+}
+
+// Metric half of kernel B on a side stream, after k_decode_bump (C already
+// bumped: c_old = C - 1 when appending): head statistics from the partials,
+// then metric[slot] += sum_h f(exp2(s - M)/Z) over the attended positions and
+// the appended slot's metric/logical/fresh (metrics.py:153-158, 189-211).
+template <int D>
+__global__ void __launch_bounds__(256) k_decode_metric(const Params P) {
+  __shared__ float Ms[kHP], iZ[kHP];
+  const kvc_pool &p = P.p;
+  const int pair = blockIdx.x, slice = blockIdx.y;
+  const int H = p.num_kv_heads, r = P.r;
+  const int bi = pair / H, head = pair % H;
+  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
+  const bool append = P.k_new != nullptr;
+  const int cp = p.ctx[hidx];
+  const int c_old = cp - (append ? 1 : 0);
+  if (cp < 1 || cp > p.nblocks[hidx] * kBlk) return;
+  const int nck = (cp + P.item_tok - 1) / P.item_tok;
+  const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < kHP) {
+    const int h = warp;
+    float M = -INFINITY;
+    for (int c = lane; c < nck; c += 32) M = fmaxf(M, __ldcg(pml + c * 2 * kHP + h));
+    M = warp_max(M);
+    float Z = 0.f;
+    for (int c = lane; c < nck; c += 32) {
+      const float m = __ldcg(pml + c * 2 * kHP + h);
+      if (m != -INFINITY) Z += __ldcg(pml + c * 2 * kHP + kHP + h) * exp2f(m - M);
+    }
+    Z = warp_sum(Z);
+    if (lane == 0) {
+      Ms[h] = M;
+      iZ[h] = Z > 0.f ? 1.f / Z : 0.f;
+    }
+  }
+  __syncthreads();
+  const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
+  const int32_t *tab = head_table(p, hidx);
+  const int nq_all = (cp + 3) / 4, qper = (nq_all + gridDim.y - 1) / gridDim.y;
+  const int q_lo = slice * qper, q_hi = q_lo + qper;
+  switch (r) {
+    case 1: metric_quads<1>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
+    case 2: metric_quads<2>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
+    case 4: metric_quads<4>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
+    default: metric_quads<8>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
   }
 }
 
@@ -785,10 +724,6 @@ int launch(Params &P, cudaStream_t s) {
   if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
   int grid = n_sm * per_sm;
   if (grid > P.n_items) grid = P.n_items;
-  // Finishing inside kernel A (one warp per pair) measured slower than the
-  // 256-thread finish kernel; KVC_K1_FUSED_FINISH=1 selects it for experiments.
-  static const bool fused_finish = getenv("KVC_K1_FUSED_FINISH") != nullptr;
-  P.fuse_finish = fused_finish ? 1 : 0;
   if (!P.counter_ready) cudaMemsetAsync(P.counter, 0, (1 + P.batch * P.p.num_kv_heads) * sizeof(int), s);
   {
     cudaLaunchConfig_t cfg = {};
@@ -821,7 +756,7 @@ int launch(Params &P, cudaStream_t s) {
             nw, (e_min - t0) / 1e3, e_mean / 1e3, (e_max - t0) / 1e3);
     free(h);
   }
-  if (!P.fuse_finish) {
+  {
     const int smem_b = (2 + P.n_ck) * kHP * 4;
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
     const int pairs_b = P.batch * P.p.num_kv_heads;
@@ -832,6 +767,20 @@ int launch(Params &P, cudaStream_t s) {
   }
   const int pairs = P.batch * P.p.num_kv_heads;
   launch_pdl(k_decode_bump, (pairs + 255) / 256, 256, 0, s, P);
+  if (P.metric_split) {
+    // fork: the metric accumulation runs beside the caller's next work on s
+    static cudaEvent_t ev[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) return KVC_ERR_UNSUPPORTED;
+    if (!ev[dev]) cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming);
+    cudaStream_t ms = reinterpret_cast<cudaStream_t>(P.metric_stream);
+    cudaEventRecord(ev[dev], s);
+    cudaStreamWaitEvent(ms, ev[dev], 0);
+    int msplit = 1184 / (pairs > 0 ? pairs : 1);
+    msplit = msplit < 1 ? 1 : msplit > 8 ? 8 : msplit;
+    k_decode_metric<D><<<dim3(pairs, msplit), 256, 0, ms>>>(P);
+  }
   return cudaGetLastError() == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
 }
 
@@ -879,6 +828,8 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.rows_stride = a->rows_stride;
   P.metric_mode = a->metric_mode;
   P.append_fresh = a->append_fresh;
+  P.metric_stream = a->metric_stream;
+  P.metric_split = (a->metric_stream && a->metric_mode && !a->rows_out && (r == 1 || r == 2 || r == 4 || r == 8)) ? 1 : 0;
   P.item_tok = item_blocks_for((int64_t)a->batch * H, max_ctx) * kBlk;
   P.max_ctx_pad = (max_ctx + P.item_tok - 1) / P.item_tok * P.item_tok;
   P.n_ck = P.max_ctx_pad / P.item_tok;

@@ -39,13 +39,16 @@ class DecodeStepGraph:
 
     def __init__(self, cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
                  seq_ids, cfg: AttentionConfig, metric_mode: int = 2, fresh: bool = True, headroom: int = 256,
-                 buffers: dict | None = None):
+                 buffers: dict | None = None, metric_overlap: bool = True):
         self.cache, self.tables, self.manager, self.store = cache, tables, manager, store
         self.seq_ids = list(seq_ids)
         self.cfg = cfg
         self.metric_mode = metric_mode
         self.fresh = fresh
         self.headroom = headroom
+        # the metric accumulation of layer m runs on a side branch of the graph
+        # beside layer m+1's attention (workspaces alternate between layers)
+        self.metric_overlap = metric_overlap and metric_mode != 0
         dev = cache.device
         self.device = dev
         B, l = len(self.seq_ids), tables.num_layers
@@ -82,9 +85,17 @@ class DecodeStepGraph:
         dec_need = lib.kvc_decode_scratch_bytes(ctypes.byref(p), B, self.cfg.num_query_heads, self.cap_ctx + 1)
         heads = B * l * H
         alloc_need = self.manager.free_tile.numel() * 8 + heads * 8 + (1 << 16)
-        self.ws = torch.empty(max(dec_need, alloc_need) + (1 << 20), dtype=torch.uint8, device=dev)
+        nws = 2 if self.metric_overlap else 1
+        self.ws = [torch.empty(max(dec_need, alloc_need) + (1 << 20), dtype=torch.uint8, device=dev)
+                   for _ in range(nws)]
         self.queue = torch.zeros(1 + B * H, dtype=torch.int32, device=dev)
-        p.scratch, p.scratch_bytes = self.ws.data_ptr(), self.ws.numel()
+        p.scratch, p.scratch_bytes = self.ws[0].data_ptr(), self.ws[0].numel()
+        pools = [p]
+        if nws == 2:
+            p1 = pool_struct(cache=self.cache, tables=t, manager=self.manager, store=self.store)
+            p1.scratch, p1.scratch_bytes = self.ws[1].data_ptr(), self.ws[1].numel()
+            pools.append(p1)
+        self.side = torch.cuda.Stream(dev) if self.metric_overlap else None
         args = []
         for m in range(l):
             a = _lib.DecodeArgs()
@@ -104,14 +115,26 @@ class DecodeStepGraph:
             a.max_ctx = self.cap_ctx + 1
             a.splits = 0
             a.queue = self.queue.data_ptr()
+            a.metric_stream = self.side.cuda_stream if self.side is not None else None
             args.append(a)
-        self._keep = (p, args)
+        self._keep = (pools, args)
 
-        def body(stream):
+        def body(s):
+            stream = s.cuda_stream
             _lib.check(lib.kvc_alloc_decode(ctypes.byref(p), self.rows_sorted_t.data_ptr(), B, self.counts.data_ptr(),
                                             stream), "alloc_decode")
-            for a in args:
-                _lib.check(lib.kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), stream), "paged_decode")
+            done = []
+            for m, a in enumerate(args):
+                if self.side is not None and m >= 2:
+                    s.wait_event(done[m - 2])  # layer m reuses layer m-2's workspace
+                _lib.check(lib.kvc_paged_decode(ctypes.byref(pools[m % len(pools)]), ctypes.byref(a), stream),
+                           "paged_decode")
+                if self.side is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(self.side)
+                    done.append(ev)
+            for ev in done[-2:]:  # join the side branch before the fresh clear
+                s.wait_event(ev)
             _lib.check(lib.kvc_clear_fresh(ctypes.byref(p), self.rows_t.data_ptr(), B, stream), "clear_fresh")
 
         self.graph = torch.cuda.CUDAGraph()
@@ -119,7 +142,7 @@ class DecodeStepGraph:
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
             with torch.cuda.graph(self.graph, stream=s):
-                body(s.cuda_stream)
+                body(s)
         torch.cuda.current_stream(dev).wait_stream(s)
         self.captured_at = self._bounds()
 
