@@ -407,8 +407,10 @@ def decode_bench(S, args, e2e=False):
             res["k1_gbs"] = float(bytes_steps.sum() / (ms * 1e-3) / 1e9)
             res["k1_timing"] = ("CUDA-graph replay: decode step time / layers, CUDA events around the timed "
                                 "steps (input copies, K0 allocation and fresh clear charged to K1)")
-        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream, finish, bump) + fresh clear
-        res["launches_per_step"] = 4 + 3 * l + 1
+        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream, finish, bump[, metric on the
+        # graph's side branch]) + fresh clear
+        per_layer = 4 if (graph is not None and graph.metric_overlap) else 3
+        res["launches_per_step"] = 4 + per_layer * l + 1
     else:
         res["h2d"] = int(sum(x.numel() * 2 for x in (hq[0], hk[0], hv[0])))
         res["d2h"] = int(hout.numel() * 2)
