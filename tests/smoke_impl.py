@@ -43,4 +43,22 @@ def run_smoke():
     got = K.compress(rig.cache, rig.tables, rig.manager, rig.store, budgets).to_dict()
     want = O.compress(st, budgets)
     assert got == want, "compress schedule differs from the oracle"
-    print("smoke: decode + compress parity ok")
+    # prefill: K/V scatter + K2 window metric (tcgen05, persistent) installed per slot
+    L, H2, r2, d2 = 300, 2, 4, 64
+    qf = bf16_round(rng.standard_normal((1, H2 * r2, L, d2)))
+    kf = bf16_round(rng.standard_normal((1, H2, L, d2)))
+    vf = bf16_round(rng.standard_normal((1, H2, L, d2)))
+    nb = H2 * (L // b + 2) + 8
+    rig2 = DevRig(nb, b, d2, 1, H2, max_seqs=2)
+    K.prefill_sequence(rig2.cache, rig2.tables, rig2.manager, rig2.store, 0, t(qf[:, :, L - 8:]), t(kf), t(vf),
+                       K.MetricConfig())
+    _lib.DeviceContext.get(rig2.cache.device).raise_status()
+    st2 = O.OracleState(nb, b, d2, 1, H2)
+    O.prefill(st2, 0, qf, kf, vf)
+    got2 = rig2.to_oracle()
+    assert np.allclose(got2.metric, st2.metric, rtol=2e-3, atol=1e-6 * st2.metric.max()), "window metric"
+    # KVC-full metric (tcgen05 row statistics + column sums)
+    full, _ = K.full_metrics(t(qf[0]), t(kf[0]), K.MetricConfig(mode="full"), H2)
+    want_full = O.full_metric(qf[0], kf[0], H2, excluded=10, aggregation="L2")
+    assert np.allclose(full.cpu().numpy(), want_full, rtol=2e-3, atol=1e-6 * want_full.max()), "full metric"
+    print("smoke: decode + compress + window/full metric parity ok")
