@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--metric-mode", type=int, default=2, help="decode metric: 2 L2 (reference default), 1 L1, 0 off")
     ap.add_argument("--no-metric-overlap", action="store_true",
                     help="graph step: accumulate the metric in the finish kernel instead of a side branch")
+    ap.add_argument("--no-fragmented", action="store_true", help="skip the random-placement decode measurement")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the decode step layer by layer instead of replaying its CUDA graph")
     ap.add_argument("--preset", default="l8b", choices=sorted(PRESETS),
@@ -417,6 +418,25 @@ def decode_bench(S, args, e2e=False):
     return res
 
 
+def fragment_placement(S, seed=7):
+    """Randomly permute the physical blocks behind every running sequence's
+    tables (post-compaction fragmentation vs sequential
+    placement).  Only the table -> block mapping changes; block contents are
+    synthetic, so decode work is identical."""
+    torch = S["torch"]
+    tables = S["tables"]
+    rows = torch.tensor([tables.row(s) for s in range(S["B"])], device=tables.tables.device).long()
+    tab = tables.tables[rows]                                   # [B, l, H, maxB]
+    nb = tables.nblocks[rows].long()
+    live = torch.arange(tab.shape[-1], device=tab.device)[None, None, None, :] < nb[..., None]
+    ids = tab[live]
+    g = torch.Generator(device=ids.device)
+    g.manual_seed(seed)
+    tab[live] = ids[torch.randperm(ids.numel(), generator=g, device=ids.device)]
+    tables.tables[rows] = tab
+    torch.cuda.synchronize()
+
+
 def decode_compression_rounds(S, args, rounds=2, gap_steps=8):
     """The engine's every-step policy (engine.py:89-93, 275-280, 360-378):
     one compress() over the whole running batch, budgets from
@@ -612,6 +632,18 @@ def main():
     dec = decode_bench(S, args)
     e2e = None if args.no_e2e else decode_bench(S, args, e2e=True)
     dcr = decode_compression_rounds(S, args)
+    # last: the same decode with every block of the batch at a random place in
+    # the pool (metadata no longer needed; the step is otherwise identical)
+    frag = None
+    if not args.no_fragmented:
+        fragment_placement(S)
+        fsteps = max(3, min(args.steps, 5))
+        fargs = argparse.Namespace(**{**vars(args), "steps": fsteps})
+        frag = decode_bench(S, fargs)
+        frag = {"value": args.batch * world * fsteps / (frag["ms"] * 1e-3), "unit": UNIT,
+                "ms_per_step": frag["ms"] / fsteps, "steps": fsteps,
+                "what": "same decode step with the batch's blocks randomly permuted over the pool "
+                        "(fragmented placement; the default line is the allocator's contiguous placement)"}
     ms = dec["ms"]
     ms_e2e = e2e["ms"] if e2e else None
     if dist is not None:
@@ -660,6 +692,7 @@ def main():
                      "bytes_per_launch": dec["k1_bytes_mean"], "launch_ms": dec["k1_ms_mean"],
                      "timing": dec["k1_timing"]},
         "eviction_step": evict,
+        "fragmented_placement": frag,
         "clocks": dec["clocks"],
         "gpu_launches": dec["launches_per_step"] * steps,
     }
