@@ -92,6 +92,13 @@ __device__ __forceinline__ void tma3d(void *dst, const CUtensorMap *map, int x, 
       : "memory");
 }
 
+// exp2 on the MUFU (ex2.approx, as in FlashAttention); -inf -> +0
+__device__ __forceinline__ float ex2f_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
@@ -343,12 +350,14 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       }
       const float mn0 = fmaxf(m0, bm0), mn1 = fmaxf(m1, bm1);
       const bool z0 = mn0 == -INFINITY, z1 = mn1 == -INFINITY;
-      const float al0 = z0 ? 1.f : exp2f(m0 - mn0);
-      const float al1 = z1 ? 1.f : exp2f(m1 - mn1);
-      const float p00 = z0 ? 0.f : exp2f(s00 - mn0);
-      const float p10 = z0 ? 0.f : exp2f(s10 - mn0);
-      const float p01 = z1 ? 0.f : exp2f(s01 - mn1);
-      const float p11 = z1 ? 0.f : exp2f(s11 - mn1);
+      const float al0 = z0 ? 1.f : ex2f_fast(m0 - mn0);
+      const float al1 = z1 ? 1.f : ex2f_fast(m1 - mn1);
+      const float p00 = z0 ? 0.f : ex2f_fast(s00 - mn0);
+      const float p10 = z0 ? 0.f : ex2f_fast(s10 - mn0);
+      const float p01 = z1 ? 0.f : ex2f_fast(s01 - mn1);
+      const float p11 = z1 ? 0.f : ex2f_fast(s11 - mn1);
+      // the output only needs rescaling when some head's running max moved
+      const bool rescale = __any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f);
       m0 = mn0;
       m1 = mn1;
       l0 = l0 * al0 + p00 + p10;
@@ -356,12 +365,17 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       const uint32_t pb0 = movmatrix_t(pack_bf16(p00, p01));
       const uint32_t pb1 = movmatrix_t(pack_bf16(p10, p11));
       const uint32_t vbase = smem_u32(vb);
+      if (rescale) {
+#pragma unroll
+        for (int mt = 0; mt < kKS; ++mt) {
+          oacc[mt][0] *= al0;
+          oacc[mt][1] *= al1;
+          oacc[mt][2] *= al0;
+          oacc[mt][3] *= al1;
+        }
+      }
 #pragma unroll
       for (int mt = 0; mt < kKS; ++mt) {
-        oacc[mt][0] *= al0;
-        oacc[mt][1] *= al1;
-        oacc[mt][2] *= al0;
-        oacc[mt][3] *= al1;
         uint32_t a0, a1, a2, a3;
         ldsm_x4_t(vbase + swz(lt_tok, 2 * mt + lt_cadd), a0, a1, a2, a3);
         mma16816(oacc[mt], a0, a1, a2, a3, pb0, pb1);
