@@ -6,7 +6,7 @@ set -x
 O=gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $O/b_ncu.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_decode_stream|k_decode_finish" -s 64 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"k_decode_stream|k_decode_finish|k_decode_metric" -s 96 -c 3 \
     -o $O/prof_k1 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $O/p1.log 2>&1
 K2_LAYERS=32 ncu --set full --clock-control none --import-source on -k regex:k_window_persist -s 1 -c 1 \
     -o $O/prof_k2 python tools/time_k2.py > $O/p2.log 2>&1
