@@ -774,9 +774,13 @@ int launch(Params &P, cudaStream_t s) {
     const int smem_b = (2 + P.n_ck) * kHP * 4;
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
     const int pairs_b = P.batch * P.p.num_kv_heads;
-    // small batches: several CTAs per (sequence, head) share the metric pass
-    int ms = 1184 / (pairs_b > 0 ? pairs_b : 1);
+    // small batches: several CTAs per (sequence, head) share the merge and
+    // the metric pass (measured best: 8 / 4-8 / 2 / 1 CTAs at 8 / 64 / 256 /
+    // >= 512 pairs; each CTA folds the head statistics itself)
+    int ms = 512 / (pairs_b > 0 ? pairs_b : 1);
     ms = ms < 1 ? 1 : ms > 8 ? 8 : ms;
+    static const int ms_forced = getenv("KVC_K1_MSPLIT") ? atoi(getenv("KVC_K1_MSPLIT")) : 0;  // experiments
+    if (ms_forced > 0) ms = ms_forced;
     launch_pdl(fb, pairs_b, 256, smem_b, s, P, ms);
   }
   const int pairs = P.batch * P.p.num_kv_heads;
@@ -791,7 +795,7 @@ int launch(Params &P, cudaStream_t s) {
     cudaStream_t ms = reinterpret_cast<cudaStream_t>(P.metric_stream);
     cudaEventRecord(ev[dev], s);
     cudaStreamWaitEvent(ms, ev[dev], 0);
-    int msplit = 1184 / (pairs > 0 ? pairs : 1);
+    int msplit = 512 / (pairs > 0 ? pairs : 1);
     msplit = msplit < 1 ? 1 : msplit > 8 ? 8 : msplit;
     k_decode_metric<D><<<dim3(pairs, msplit), 256, 0, ms>>>(P);
   }
