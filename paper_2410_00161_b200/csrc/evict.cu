@@ -54,6 +54,7 @@ struct EvictState {
   int64_t *E;         // [n_seqs] clamped budget (0 = inactive)
   int64_t *seq_moves; // [n_seqs] move slots of the sequence, then its base offset
   unsigned long long *cand;  // nullable [T][2][kCand]: (key << 32 | secondary) of keys < T* / == T*
+  unsigned long long *trace; // debug (KVC_K4_TRACE): [T][8] phase stamps of k_compact16
   int64_t max_slots;
   int hp;
   int32_t *status;
@@ -809,6 +810,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
   int32_t *tab = head_table(p, hidx);
   const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
 
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 0] = t_; }
   // ---- threshold T_h = (16 e)-th smallest key; shortcut when it is T* ----
   const uint32_t Tstar = S.prefix[si];
   const int64_t lt = S.ltc[g], le = S.lec[g];
@@ -827,6 +829,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
       for (int i = 0; i < 4; ++i) ok[i] = pos + i < n && v[i] < Tstar;
     }, &tie_rank, &tie_cnt);
   }
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 1] = t_; }
   // ---- tie cut: ties at T ordered by (occupied, logical, position) ----
   auto sec = [&](int64_t pos, int32_t lg) -> uint32_t {
     return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
@@ -851,6 +854,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
     }, &dummy, &dummy2);
   }
 
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 2] = t_; }
   // ---- MoveCache pairing (holes ascending below R0, survivors descending) ----
   const int rb = nb - e;  // first block of the eviction range
   int32_t *mv = M.moves + M.move_off[g] * 2;
@@ -946,14 +950,37 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
     return;
   }
-  for (int k = threadIdx.x; k < nmoves; k += NT) {
-    const int64_t src = mv[2 * k], dst = mv[2 * k + 1];
-    p.metric[dst] = p.metric[src];
-    p.logical[dst] = p.logical[src];
-    p.protected_[dst] = p.protected_[src];
-    p.fresh[dst] = p.fresh[src];
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 3] = t_; }
+  for (int k0 = threadIdx.x; k0 < nmoves; k0 += 4 * NT) {  // four moves' loads in flight per thread
+    int64_t src[4], dst[4];
+    float mt[4];
+    int32_t lg[4];
+    uint8_t pr[4], fr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u * NT;
+      src[u] = k < nmoves ? mv[2 * k] : -1;
+      dst[u] = k < nmoves ? mv[2 * k + 1] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (src[u] >= 0) {
+        mt[u] = p.metric[src[u]];
+        lg[u] = p.logical[src[u]];
+        pr[u] = p.protected_[src[u]];
+        fr[u] = p.fresh[src[u]];
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (src[u] >= 0) {
+        p.metric[dst[u]] = mt[u];
+        p.logical[dst[u]] = lg[u];
+        p.protected_[dst[u]] = pr[u];
+        p.fresh[dst[u]] = fr[u];
+      }
   }
   __syncthreads();
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 4] = t_; }
   // ---- free the trailing e blocks and reset their slots ----
   for (int t = threadIdx.x; t < e; t += NT) {
     const int j = rb + t;
@@ -987,6 +1014,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
   }
   const int keep = rb;
   const int Cn = C < keep * 16 ? C : keep * 16;
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 5] = t_; }
   // ---- logical renumbering: rank among the kept logicals ----
   const int words = (int)((n + 31) / 32);
   uint32_t *wpre = bitmap + words;
@@ -1044,6 +1072,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
       lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
     }
   }
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 6] = t_; }
   if (threadIdx.x == 0) {
     p.nblocks[hidx] = keep;
     p.ctx[hidx] = Cn;
@@ -1690,6 +1719,7 @@ static bool small_heads(const EvictState &S) { return S.max_slots <= 8192; }
 
 int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, EvictState &S) {
   S.hp = pool->num_layers * pool->num_kv_heads;
+  S.trace = nullptr;
   S.max_slots = (a->max_slots_per_head + 3) & ~int64_t(3);  // uint4 key rows
   S.status = pool->status;
   const int64_t T = (int64_t)a->n_seqs * S.hp;
@@ -1768,6 +1798,31 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
     }
     if (small_heads(S)) {
       k_compact_warp<<<(unsigned)((T + kWC - 1) / kWC), kWC * 32, 0, s>>>(*pool, a->seq_rows, S, M, T);
+    } else if (getenv("KVC_K4_TRACE")) {
+      // debug: per-phase time of k_compact16 averaged over the heads (synchronises)
+      unsigned long long *tr = nullptr;
+      cudaMalloc(&tr, T * 64);
+      cudaMemsetAsync(tr, 0, T * 64, s);
+      S.trace = tr;
+      k_compact16<512><<<(int)T, 512, dyn, s>>>(*pool, a->seq_rows, S, M);
+      S.trace = nullptr;
+      unsigned long long *h = (unsigned long long *)malloc(T * 64);
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, tr, T * 64, cudaMemcpyDeviceToHost);
+      double acc[7] = {0};
+      unsigned long long t0 = ~0ull, t1 = 0;
+      int n = 0;
+      for (int64_t g = 0; g < T; ++g) {
+        if (!h[g * 8 + 6]) continue;
+        ++n;
+        t0 = h[g * 8] < t0 ? h[g * 8] : t0;
+        t1 = h[g * 8 + 6] > t1 ? h[g * 8 + 6] : t1;
+        for (int k = 0; k < 6; ++k) acc[k] += (double)(h[g * 8 + k + 1] - h[g * 8 + k]) / 1e3;
+      }
+      fprintf(stderr, "[k4 trace] heads %d span %.1f us; per head: T_h %.1f tie %.1f pairing %.1f meta %.1f free %.1f renumber %.1f us\n",
+              n, (t1 - t0) / 1e3, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+      free(h);
+      cudaFree(tr);
     }
     else if (dyn <= 100 * 1024) k_compact16<512><<<(int)T, 512, dyn, s>>>(*pool, a->seq_rows, S, M);
     else return KVC_ERR_UNSUPPORTED;
