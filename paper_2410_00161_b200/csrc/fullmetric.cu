@@ -33,7 +33,7 @@ constexpr int kEpiW = 8;
 constexpr int kFThreads = 64 + 32 * kEpiW;
 
 template <int D>
-constexpr int full_stages() { return D >= 128 ? 4 : 8; }
+constexpr int full_stages() { return D >= 128 ? 2 : 4; }  // 2 CTAs per SM (2 x 256 TMEM columns)
 
 struct FullParams {
   int L, n_q, H, r, v;  // v = excluded query window
@@ -71,7 +71,7 @@ __device__ __forceinline__ void mma_tile(uint32_t tmem_d, uint32_t abase, uint32
 // F1: row statistics.  CTA = (query tile, query head), heaviest tiles first.
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(kFThreads, 1)
+__global__ void __launch_bounds__(kFThreads, 2)
     k_full_stats(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, const FullParams P) {
   constexpr int kStages = full_stages<D>();
   constexpr int kTileBytes = kT * D * 2;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // stream is the group's r query heads x query tiles with rows >= j0 + v.
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(kFThreads, 1)
+__global__ void __launch_bounds__(kFThreads, 2)
     k_full_colsum(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, const FullParams P) {
   constexpr int kStages = full_stages<D>();
   constexpr int kTileBytes = kT * D * 2;
