@@ -681,6 +681,14 @@ def main():
             "ms": dcr["ms"], "freed_blocks": dcr["freed"],
             "ratio_to_decode_step": dcr["ms"][-1] / step_ms},
     }
+    if ev["fused_ms"]:
+        # on-prefill policy: the metric -> schedule -> compact step fused into the
+        # prompt write, minus the plain prompt write it replaces (can be < 0)
+        fused = float(np.mean(ev["fused_ms"][timed]))
+        scat = float(np.mean(ev["scatter_ms"][timed]))
+        evict["fused_marginal_over_prompt_write"] = {
+            "ms_per_sequence": fused - scat, "ratio_to_decode_step": (fused - scat) / step_ms,
+            "what": "prefill_compress_sequence minus write_prefill_kv_layers for the same prompt"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
