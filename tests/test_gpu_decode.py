@@ -232,3 +232,36 @@ def test_append_lookup_round_trip():
         assert np.array_equal(v.double().cpu().numpy(), vals[pos])
     assert K.fragmentation(rig.tables) == sum(
         (-(-len(kv[0]) // 4)) * 4 - len(kv[0]) for kv in written.values())
+
+
+def test_decode_bench_scale_path():
+    """The bench's launch configuration: 64 sequences x 8 KV heads (512 pairs)
+    with ~1.2-1.6k ragged contexts selects 256-position split-KV items and one
+    finish CTA per (sequence, head); a fragmented pool.  Two layers, one
+    decode step each, vs the oracle."""
+    rng = np.random.default_rng(64)
+    b, d, heads, r, layers = 16, 64, 8, 4, 2
+    seqs = list(range(64))
+    # random_state pre-takes ~30% of the pool to fragment it: size for that
+    nblocks = int(len(seqs) * layers * heads * (1700 // b + 2) * 1.6) + 64
+    st = random_state(rng, nblocks, b, d, layers, heads, seqs, 1600, min_len=1200)
+    rig = DevRig(nblocks, b, d, layers, heads, max_seqs=72, max_blocks=1700 // b + 8)
+    rig.load(st)
+    cfg = K.AttentionConfig(heads * r, heads, d, layers)
+    assert rig.manager.allocate_decode_step(seqs) == O.alloc_decode(st, seqs)
+    dev = rig.cache.device
+    for layer in range(layers):
+        q = bf16_round(rng.standard_normal((len(seqs), heads * r, d)))
+        kn = bf16_round(rng.standard_normal((len(seqs), heads, d)))
+        vn = bf16_round(rng.standard_normal((len(seqs), heads, d)))
+        out = K.paged_decode(torch.from_numpy(q).to(dev, torch.bfloat16), rig.cache, rig.tables, seqs, layer, cfg,
+                             store=rig.store, metric_mode=2, k_new=torch.from_numpy(kn).to(dev, torch.bfloat16),
+                             v_new=torch.from_numpy(vn).to(dev, torch.bfloat16), out_f32=True).cpu().numpy()
+        for i, s in enumerate(seqs):
+            ref_out, _ = O.decode_step_layer(st, s, layer, q[i], kn[i], vn[i], "L2")
+            assert np.abs(out[i] - ref_out).max() < OUT_ATOL, (layer, s)
+    from paper_2410_00161_b200 import _lib
+    _lib.DeviceContext.get(dev).raise_status()
+    dst = rig.to_oracle()
+    assert_same_ints(dst, st)
+    assert np.allclose(dst.metric, st.metric, rtol=MET_RTOL, atol=1e-6)
