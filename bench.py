@@ -400,7 +400,7 @@ def decode_bench(S, args, e2e=False):
             durs = np.array([a.elapsed_time(z) for a, z in layer_events]).reshape(steps, l)
             res["k1_ms_mean"] = float(durs.mean())
             res["k1_gbs"] = float(bytes_steps.sum() / (durs.sum() * 1e-3) / 1e9)
-            res["k1_timing"] = "CUDA events around each layer's launches (stream, finish, bump) on the launching stream"
+            res["k1_timing"] = "CUDA events around each layer's launches (stream, finish) on the launching stream"
         else:
             # inside the replay a layer cannot be bracketed by events: charge K1
             # the whole step (input copies, allocation and fresh clear included)
@@ -408,9 +408,9 @@ def decode_bench(S, args, e2e=False):
             res["k1_gbs"] = float(bytes_steps.sum() / (ms * 1e-3) / 1e9)
             res["k1_timing"] = ("CUDA-graph replay: decode step time / layers, CUDA events around the timed "
                                 "steps (input copies, K0 allocation and fresh clear charged to K1)")
-        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream, finish, bump[, metric on the
+        # K0 (decode demand, tile scan, tile take, bind) + per layer K1 (stream, finish[, metric on the
         # graph's side branch]) + fresh clear
-        per_layer = 4 if (graph is not None and graph.metric_overlap) else 3
+        per_layer = 3 if (graph is not None and graph.metric_overlap) else 2
         res["launches_per_step"] = 4 + per_layer * l + 1
     else:
         res["h2d"] = int(sum(x.numel() * 2 for x in (hq[0], hk[0], hv[0])))

@@ -113,6 +113,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// store with an L2 eviction-priority hint (scratch that is read back soon)
+__device__ __forceinline__ void st_hint(float *a, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+
+// drop a 128-byte L2 line without writing it back (scratch fully consumed;
+// `a` 128-byte aligned)
+__device__ __forceinline__ void discard_l2(const void *a) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Warp reductions
 // ---------------------------------------------------------------------------

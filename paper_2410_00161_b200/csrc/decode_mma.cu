@@ -67,9 +67,10 @@ struct Params {
   int n_ck;         // chunks per (sequence, head) upper bound
   int n_items;
   float scale;      // log2(e)/sqrt(d)
-  int *counter;     // work queue head (reset by k_decode_bump for the next call)
-  int *pair_done;   // [pairs] reserved per-pair counters (kept zero by k_decode_bump)
+  int *counter;     // work queue head (reset by kernel B for the next call)
+  int *pair_done;   // [pairs] kernel B arrival counters (left zero by the last CTA of the pair)
   int metric_split; // 1: kernel B writes the output only; k_decode_metric (side stream) accumulates
+  int need_scores;  // a metric or rows pass reads the score row (else kernel A skips it)
   void *metric_stream;
   int counter_ready;
   float *scores;    // [pairs][max_ctx_pad][r]
@@ -78,7 +79,7 @@ struct Params {
   unsigned long long *trace;  // debug (KVC_K1_TRACE): [grid*warps][2] start/end globaltimer
 };
 
-// Programmatic dependent launch: the finish and bump kernels are launched
+// Programmatic dependent launch: the finish kernel (and the next stream) is launched
 // while kernel A drains; they block here until A's writes are visible.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -190,28 +191,6 @@ __device__ void fetch_item(const Params &P, WItem &w, int lane) {
   __syncwarp();
 }
 
-// After kernel A: status checks for heads that produced no item, C += 1 for
-// appends, and the queue / per-pair counters reset for the next launch.
-__global__ void k_decode_bump(const Params P) {
-  const kvc_pool &p = P.p;
-  const int H = p.num_kv_heads;
-  const int pairs = P.batch * H;
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) *P.counter = 0;
-  if (i >= pairs) return;
-  P.pair_done[i] = 0;
-  const int bi = i / H, head = i % H;
-  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
-  const int c_old = p.ctx[hidx];
-  const bool append = P.k_new != nullptr;
-  const int cp = c_old + (append ? 1 : 0);
-  if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
-  else if (cp > p.nblocks[hidx] * kBlk) set_status(p.status, append ? KVC_DEV_ALLOCATION_ORDER : KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, c_old);
-  else if (append) p.ctx[hidx] = c_old + 1;
-}
-
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constant__ CUtensorMap tmK,
                                                            const __grid_constant__ CUtensorMap tmV,
@@ -247,6 +226,9 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
   pdl_wait();     // the previous kernel's writes (ctx, tables, q, queue) are visible
   pdl_trigger();  // let kernel B's CTAs launch and park in griddepcontrol.wait
   const uint64_t pol = policy_evict_first();
+  // scores and partials are read back within the layer: keep them in L2
+  // (their readers discard the lines, so they never reach HBM)
+  const uint64_t pol_keep = policy_evict_last();
   fetch_item(P, wit[0], lane);
   fetch_item(P, wit[1], lane);
 
@@ -334,13 +316,13 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       const float s01 = (tv0 && hv1) ? sc[1] * P.scale : -INFINITY;
       const float s10 = (tv1 && hv0) ? sc[2] * P.scale : -INFINITY;
       const float s11 = (tv1 && hv1) ? sc[3] * P.scale : -INFINITY;
-      {
+      if (P.need_scores) {
         float *r0 = srow_base + (int64_t)(tb0 + g) * r;
         float *r1 = r0 + 8 * r;
-        if (tv0 && hv0) r0[2 * t] = s00;
-        if (tv0 && hv1) r0[2 * t + 1] = s01;
-        if (tv1 && hv0) r1[2 * t] = s10;
-        if (tv1 && hv1) r1[2 * t + 1] = s11;
+        if (tv0 && hv0) st_hint(r0 + 2 * t, s00, pol_keep);
+        if (tv0 && hv1) st_hint(r0 + 2 * t + 1, s01, pol_keep);
+        if (tv1 && hv0) st_hint(r1 + 2 * t, s10, pol_keep);
+        if (tv1 && hv1) st_hint(r1 + 2 * t + 1, s11, pol_keep);
       }
       float bm0 = fmaxf(s00, s10), bm1 = fmaxf(s01, s11);
 #pragma unroll
@@ -402,12 +384,12 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
 #pragma unroll
     for (int mt = 0; mt < kKS; ++mt) {
       if (hv0) {
-        po[(2 * t) * D + mt * 16 + g] = oacc[mt][0];
-        po[(2 * t) * D + mt * 16 + g + 8] = oacc[mt][2];
+        st_hint(po + (2 * t) * D + mt * 16 + g, oacc[mt][0], pol_keep);
+        st_hint(po + (2 * t) * D + mt * 16 + g + 8, oacc[mt][2], pol_keep);
       }
       if (hv1) {
-        po[(2 * t + 1) * D + mt * 16 + g] = oacc[mt][1];
-        po[(2 * t + 1) * D + mt * 16 + g + 8] = oacc[mt][3];
+        st_hint(po + (2 * t + 1) * D + mt * 16 + g, oacc[mt][1], pol_keep);
+        st_hint(po + (2 * t + 1) * D + mt * 16 + g + 8, oacc[mt][3], pol_keep);
       }
     }
     (void)item_id;
@@ -479,86 +461,31 @@ __device__ __forceinline__ void metric_quads(const Params &P, const float *srow,
   }
 }
 
-// Kernel B: per (sequence, head): merge partials, output, metric, C += 1.
-template <int D>
-__global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
-  extern __shared__ float sm[];
-  float *Ms = sm, *iZ = sm + kHP, *fac = sm + 2 * kHP;  // fac: [n_ck][kHP]
-  const kvc_pool &p = P.p;
-  const int pair = blockIdx.x;
-  const int slice = blockIdx.y;  // key slice of the metric pass; slice 0 also writes the output
-  const int H = p.num_kv_heads, r = P.r, n_q = H * r;
-  const int bi = pair / H, head = pair % H;
-  pdl_wait();
-  pdl_trigger();
-  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
-  const int c_old = p.ctx[hidx];
-  const bool append = P.k_new != nullptr;
-  const int cp = c_old + (append ? 1 : 0);
-  if (slice == 0) {
-    // NumericError: non-finite query (attention.py:33-36, 108)
-    const uint16_t *qg = P.q + ((int64_t)bi * n_q + head * r) * D;
-    bool bad = false;
-    for (int e = threadIdx.x; e < r * D; e += blockDim.x) bad |= !isfinite(bf16_bits_to_f32(qg[e]));
-    if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
-  }
-  if (cp < 1 || cp > p.nblocks[hidx] * kBlk) return;  // reported by k_decode_bump
-  const int nck = (cp + P.item_tok - 1) / P.item_tok;
-  const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // head statistics: warp h folds head h's partials (lanes stride the chunks),
-  // then the merge factors fac[c][h] = exp2(m_c - M_h)
-  if (warp < kHP) {
-    const int h = warp;
-    float M = -INFINITY;
-    for (int c = lane; c < nck; c += 32) M = fmaxf(M, __ldcg(pml + c * 2 * kHP + h));
-    M = warp_max(M);
-    float Z = 0.f;
-    for (int c = lane; c < nck; c += 32) {
-      const float m = __ldcg(pml + c * 2 * kHP + h);
-      const float f = m == -INFINITY ? 0.f : exp2f(m - M);
-      fac[c * kHP + h] = f;
-      Z += __ldcg(pml + c * 2 * kHP + kHP + h) * f;
-    }
-    Z = warp_sum(Z);
-    if (lane == 0) {
-      Ms[h] = M;
-      iZ[h] = Z > 0.f ? 1.f / Z : 0.f;
-    }
-  }
+// After this CTA's metric pass: drop its score lines [q_lo, q_hi) quads
+// (q_lo a multiple of 8 quads = 128*r bytes) from L2 without a write-back.
+__device__ __forceinline__ void discard_scores(const float *srow, int r, int nq_all, int q_lo, int q_hi) {
+  const int q_end = min(nq_all, q_hi);
+  if (q_end <= q_lo) return;
   __syncthreads();
-  // output: the CTAs of the pair share the r*D outputs; with few outputs per
-  // CTA, TPO adjacent lanes split one output's chunk partials (fixed order)
-  {
-    const float *po = P.part_o + (int64_t)pair * P.n_ck * r * D;
-    const int E = r * D;
-    const int per = (E + gridDim.y - 1) / gridDim.y;
-    const int e_lo = slice * per, e_hi = min(E, e_lo + per);
-    int tpo = 1;
-    while (tpo < 32 && (e_hi - e_lo) * tpo * 2 <= (int)blockDim.x) tpo *= 2;
-    const int sub = threadIdx.x % tpo;
-    for (int e0 = e_lo + (int)threadIdx.x / tpo; e0 < e_lo + ((e_hi - e_lo + (int)blockDim.x / tpo - 1) / ((int)blockDim.x / tpo)) * ((int)blockDim.x / tpo); e0 += blockDim.x / tpo) {
-      const bool real = e0 < e_hi;
-      const int e = real ? e0 : e_lo;
-      const int h = e / D;
-      float acc4[4] = {0.f, 0.f, 0.f, 0.f};
-      int c = sub, u = 0;
-      for (; c < nck; c += tpo, u = (u + 1) & 3) acc4[u] += __ldcg(po + (int64_t)c * E + e) * fac[c * kHP + h];
-      float s = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-      for (int o = 1; o < tpo; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (real && sub == 0) {
-        const float o = s * iZ[h];
-        const int64_t oi = ((int64_t)bi * n_q + head * r) * D + e;
-        if (P.out_f32) reinterpret_cast<float *>(P.out)[oi] = o;
-        else reinterpret_cast<__nv_bfloat16 *>(P.out)[oi] = __float2bfloat16(o);
-      }
-    }
-  }
-  if (P.metric_split) return;  // k_decode_metric accumulates on the side stream
+  const char *b = reinterpret_cast<const char *>(srow + (int64_t)q_lo * 4 * r);
+  const int lines = ((q_end - q_lo) * 16 * r + 127) / 128;
+  for (int i = threadIdx.x; i < lines; i += blockDim.x) discard_l2(b + (int64_t)i * 128);
+}
+
+// Metric / rows pass of kernel B when no side stream takes it: sum over the
+// r heads of f(exp2(s - M) / Z) into metric[slot] for this CTA's key slice,
+// the appended slot initialised (metrics.py:153-158, 189-211).
+__device__ void finish_metric(const Params &P, int pair, int slice, int64_t hidx, int cp, int c_old, bool append,
+                              const float *Ms, const float *iZ) {
+  const kvc_pool &p = P.p;
+  const int H = p.num_kv_heads, r = P.r;
+  const int bi = pair / H, head = pair % H;
   // metric / rows over all attended positions
   const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
   const int32_t *tab = head_table(p, hidx);
-  const int nq_all = (cp + 3) / 4, qper = (nq_all + gridDim.y - 1) / gridDim.y;
+  // key slices in whole 8-quad units, so no 128-byte score line is shared
+  // between CTAs (each CTA discards its own lines)
+  const int nq_all = (cp + 3) / 4, qper = ((nq_all + gridDim.y - 1) / gridDim.y + 7) & ~7;
   const int q_lo = slice * qper, q_hi = q_lo + qper;
   if (P.metric_mode && !P.rows_out && (r == 1 || r == 2 || r == 4 || r == 8)) {
     switch (r) {
@@ -567,6 +494,7 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
       case 4: metric_quads<4>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
       default: metric_quads<8>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
     }
+    discard_scores(srow, r, nq_all, q_lo, q_hi);
   } else if (P.metric_mode || P.rows_out) {
     for (int pos = q_lo * 4 + threadIdx.x; pos < min(cp, q_hi * 4); pos += blockDim.x) {
       float contrib = 0.f;
@@ -597,7 +525,166 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   }
 }
 
-// Metric half of kernel B on a side stream, after k_decode_bump (C already
+// Kernel B: per (sequence, head): merge partials, output, metric, C += 1,
+// and the queue reset for the next launch (the former k_decode_bump).
+template <int D>
+__global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
+  extern __shared__ float sm[];
+  float *Ms = sm, *iZ = sm + kHP, *fac = sm + 2 * kHP;  // fac: [n_ck][kHP]
+  const kvc_pool &p = P.p;
+  const int pair = blockIdx.x;
+  const int slice = blockIdx.y;  // key slice of the metric pass / share of the outputs
+  const int H = p.num_kv_heads, r = P.r, n_q = H * r;
+  const int bi = pair / H, head = pair % H;
+  // Prologue before the dependency wait: kernel A writes none of these
+  // (it only reads ctx/tables/q), so they overlap A's tail.
+  const int64_t hidx = head_index(p, P.rows[bi], P.layer, head);
+  const int c_old = p.ctx[hidx];
+  const bool append = P.k_new != nullptr;
+  const int cp = c_old + (append ? 1 : 0);
+  const int cap = p.nblocks[hidx] * kBlk;
+  bool bad = false;  // NumericError: non-finite query (attention.py:33-36, 108)
+  if (slice == 0) {
+    const uint16_t *qg = P.q + ((int64_t)bi * n_q + head * r) * D;
+    for (int e = threadIdx.x; e < r * D; e += blockDim.x) bad |= !isfinite(bf16_bits_to_f32(qg[e]));
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (pair == 0 && slice == 0 && threadIdx.x == 0) *P.counter = 0;  // queue head for the next launch
+  if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
+  if (cp < 1 || cp > cap) {  // no item ran for this head
+    if (slice == 0 && threadIdx.x == 0) {
+      if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
+      else set_status(p.status, append ? KVC_DEV_ALLOCATION_ORDER : KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, c_old);
+    }
+    return;
+  }
+  const int nck = (cp + P.item_tok - 1) / P.item_tok;
+  const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // output share of this CTA in float4 groups; TPO adjacent lanes split one
+  // group's chunk partials (fixed order).  The first 8 chunks' loads are in
+  // flight while the head statistics are folded.
+  constexpr int kCB = 8;
+  const int E4 = r * D / 4;
+  const int per = ((E4 + gridDim.y - 1) / gridDim.y + 7) & ~7;  // whole 128-byte lines per CTA
+  const int g_lo = slice * per, g_hi = min(E4, g_lo + per);
+  int tpo = 1;
+  while (tpo < 32 && (g_hi - g_lo) * tpo * 2 <= (int)blockDim.x) tpo *= 2;
+  const int sub = threadIdx.x % tpo;
+  const int gi = g_lo + (int)threadIdx.x / tpo;
+  const bool greal = gi < g_hi;
+  const float4 *po4 = reinterpret_cast<const float4 *>(P.part_o + (int64_t)pair * P.n_ck * r * D) + (greal ? gi : 0);
+  float4 v[kCB];
+#pragma unroll
+  for (int j = 0; j < kCB; ++j) {
+    const int c = sub + j * tpo;
+    v[j] = (greal && c < nck) ? __ldcg(po4 + (int64_t)c * E4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // head statistics: warp h folds head h's chunk partials in one pass
+  // (lane-local online max), then fac[c][h] = exp2(m_c - M_h)
+  if (warp < r) {
+    const int h = warp;
+    float mloc = -INFINITY, zloc = 0.f;
+    for (int c = lane; c < nck; c += 32) {
+      const float m = __ldcg(pml + c * 2 * kHP + h), l = __ldcg(pml + c * 2 * kHP + kHP + h);
+      fac[c * kHP + h] = m;
+      if (m != -INFINITY) {
+        if (m > mloc) {
+          zloc = zloc * ex2f_fast(mloc - m) + l;
+          mloc = m;
+        } else {
+          zloc += l * ex2f_fast(m - mloc);
+        }
+      }
+    }
+    const float M = warp_max(mloc);
+    const float Z = warp_sum(M == -INFINITY || mloc == -INFINITY ? 0.f : zloc * exp2f(mloc - M));
+    __syncwarp();
+    for (int c = lane; c < nck; c += 32) {
+      const float m = fac[c * kHP + h];
+      fac[c * kHP + h] = m == -INFINITY ? 0.f : exp2f(m - M);
+    }
+    if (lane == 0) {
+      Ms[h] = M;
+      iZ[h] = Z > 0.f ? 1.f / Z : 0.f;
+    }
+  }
+  __syncthreads();
+  {
+    const int h = greal ? gi * 4 / D : 0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = sub;; c0 += kCB * tpo) {
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) {
+        const int c = c0 + j * tpo;
+        const float f = c < nck ? fac[c * kHP + h] : 0.f;
+        acc.x += v[j].x * f, acc.y += v[j].y * f, acc.z += v[j].z * f, acc.w += v[j].w * f;
+      }
+      if (c0 + kCB * tpo >= nck) break;
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) {
+        const int c = c0 + (kCB + j) * tpo;
+        v[j] = (greal && c < nck) ? __ldcg(po4 + (int64_t)c * E4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    for (int o = 1; o < tpo; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+      acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+    }
+    if (greal && sub == 0) {
+      const float z = iZ[h];
+      const int64_t oi = ((int64_t)bi * n_q + head * r) * D + (int64_t)gi * 4;
+      if (P.out_f32) {
+        float *o = reinterpret_cast<float *>(P.out) + oi;
+        const float4 ov = make_float4(acc.x * z, acc.y * z, acc.z * z, acc.w * z);
+        if ((reinterpret_cast<uintptr_t>(o) & 15) == 0) *reinterpret_cast<float4 *>(o) = ov;
+        else o[0] = ov.x, o[1] = ov.y, o[2] = ov.z, o[3] = ov.w;
+      } else {
+        __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + oi;
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * z, acc.y * z);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * z, acc.w * z);
+        if ((reinterpret_cast<uintptr_t>(o) & 7) == 0) {
+          uint2 u;
+          u.x = *reinterpret_cast<const uint32_t *>(&lo);
+          u.y = *reinterpret_cast<const uint32_t *>(&hi);
+          *reinterpret_cast<uint2 *>(o) = u;
+        } else {
+          o[0] = lo.x, o[1] = lo.y, o[2] = hi.x, o[3] = hi.y;
+        }
+      }
+    }
+  }
+  // the chunk partials are consumed: drop this CTA's lines from L2
+  if (g_hi > g_lo) {
+    __syncthreads();
+    const int lpc = (g_hi - g_lo) / 8;
+    const char *b0 = reinterpret_cast<const char *>(P.part_o + (int64_t)pair * P.n_ck * r * D) + (int64_t)g_lo * 16;
+    for (int i = threadIdx.x; i < nck * lpc; i += blockDim.x)
+      discard_l2(b0 + (int64_t)(i / lpc) * E4 * 16 + (int64_t)(i % lpc) * 128);
+  }
+  if (!P.metric_split) finish_metric(P, pair, slice, hidx, cp, c_old, append, Ms, iZ);
+  // C += 1 once every CTA of the pair has read C (the last to arrive bumps;
+  // k_decode_metric on the side stream runs after this kernel and sees C + 1)
+  if (append) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (gridDim.y == 1) {
+        p.ctx[hidx] = c_old + 1;
+      } else {
+        __threadfence();
+        if (atomicAdd(&P.pair_done[pair], 1) == (int)gridDim.y - 1) {
+          P.pair_done[pair] = 0;
+          p.ctx[hidx] = c_old + 1;
+        }
+      }
+    }
+  }
+}
+
+// Metric half of kernel B on a side stream, after kernel B (C already
 // bumped: c_old = C - 1 when appending): head statistics from the partials,
 // then metric[slot] += sum_h f(exp2(s - M)/Z) over the attended positions and
 // the appended slot's metric/logical/fresh (metrics.py:153-158, 189-211).
@@ -635,7 +722,7 @@ __global__ void __launch_bounds__(256) k_decode_metric(const Params P) {
   __syncthreads();
   const float *srow = P.scores + (int64_t)pair * P.max_ctx_pad * r;
   const int32_t *tab = head_table(p, hidx);
-  const int nq_all = (cp + 3) / 4, qper = (nq_all + gridDim.y - 1) / gridDim.y;
+  const int nq_all = (cp + 3) / 4, qper = ((nq_all + gridDim.y - 1) / gridDim.y + 7) & ~7;
   const int q_lo = slice * qper, q_hi = q_lo + qper;
   switch (r) {
     case 1: metric_quads<1>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
@@ -643,6 +730,7 @@ __global__ void __launch_bounds__(256) k_decode_metric(const Params P) {
     case 4: metric_quads<4>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
     default: metric_quads<8>(P, srow, tab, Ms, iZ, cp, c_old, append, q_lo, q_hi); break;
   }
+  discard_scores(srow, r, nq_all, q_lo, q_hi);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -784,7 +872,6 @@ int launch(Params &P, cudaStream_t s) {
     launch_pdl(fb, pairs_b, 256, smem_b, s, P, ms);
   }
   const int pairs = P.batch * P.p.num_kv_heads;
-  launch_pdl(k_decode_bump, (pairs + 255) / 256, 256, 0, s, P);
   if (P.metric_split) {
     // fork: the metric accumulation runs beside the caller's next work on s
     static cudaEvent_t ev[64] = {};
@@ -847,6 +934,7 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.metric_mode = a->metric_mode;
   P.append_fresh = a->append_fresh;
   P.metric_stream = a->metric_stream;
+  P.need_scores = (a->metric_mode || a->rows_out) ? 1 : 0;
   P.metric_split = (a->metric_stream && a->metric_mode && !a->rows_out && (r == 1 || r == 2 || r == 4 || r == 8)) ? 1 : 0;
   P.item_tok = item_blocks_for((int64_t)a->batch * H, max_ctx) * kBlk;
   P.max_ctx_pad = (max_ctx + P.item_tok - 1) / P.item_tok * P.item_tok;
@@ -855,7 +943,7 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   P.scale = 1.4426950408889634f / sqrtf((float)D);
   char *base = reinterpret_cast<char *>(pool->scratch);
   // work-queue head + per-pair counters: the caller's persistent zeroed
-  // array (left zero by k_decode_bump), else a scratch copy zeroed per launch
+  // array (left zero by kernel B), else a scratch copy zeroed per launch
   P.counter = a->queue ? a->queue : reinterpret_cast<int *>(base);
   P.pair_done = P.counter + 1;
   P.counter_ready = a->queue ? 1 : 0;
