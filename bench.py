@@ -15,7 +15,8 @@ A decode step = K0 block allocation + 32 x K1 (fused append + paged GQA
 attention + L2 metric accumulation) + clearing the step's fresh shields.
 `value` = tokens/s with all inputs resident in HBM; `e2e` = the same step
 through the public API with queries/new KV copied from pinned host memory
-and the attention output copied back every step.  KV (>34 GB) is far larger
+and the attention output copied back every step (`DecodeStepGraph(host_io=)`:
+per layer, inside the captured step, overlapping the other layers' attention).  KV (>34 GB) is far larger
 than L2, so no flush is needed.
 """
 
@@ -323,6 +324,7 @@ def decode_bench(S, args, e2e=False):
         hk = [x.cpu().pin_memory() for x in kn]
         hv = [x.cpu().pin_memory() for x in vn]
         hout = torch.empty(out.shape, dtype=torch.bfloat16).pin_memory()
+        houts = [hout] + [torch.empty(out.shape, dtype=torch.bfloat16).pin_memory() for _ in range(n_sets - 1)]
         dq, dk, dv = torch.empty_like(q[0]), torch.empty_like(kn[0]), torch.empty_like(vn[0])
     ctx_host = tables.ctx[rows_t.long()].cpu().numpy().astype(np.int64).reshape(-1)  # [B*l*H]
     layer_events = []
@@ -330,24 +332,24 @@ def decode_bench(S, args, e2e=False):
     # as one CUDA graph; its static input buffers are written every step
     graph = None
     if not args.no_graph:
+        # e2e: the graph uploads each layer's Q/K/V from the pinned host set and
+        # downloads its output inside the step, overlapped with the other layers
+        host_io = ([{"q": hq[i], "k_new": hk[i], "v_new": hv[i], "out": houts[i]} for i in range(n_sets)]
+                   if e2e else None)
         graph = K.DecodeStepGraph(cache, tables, manager, store, seqs, cfg, metric_mode=args.metric_mode,
                                   headroom=max(64, args.steps + args.warmup + 8),
-                                  metric_overlap=not args.no_metric_overlap)
+                                  metric_overlap=not args.no_metric_overlap, host_io=host_io)
 
     def one_step(i, timed):
         sel = i % n_sets
         if graph is not None:
             if e2e:
-                graph.q.copy_(hq[sel], non_blocking=True)
-                graph.k_new.copy_(hk[sel], non_blocking=True)
-                graph.v_new.copy_(hv[sel], non_blocking=True)
-            else:
-                graph.q.copy_(q[sel])
-                graph.k_new.copy_(kn[sel])
-                graph.v_new.copy_(vn[sel])
-            res_out = graph.step()
-            if e2e:
-                hout.copy_(res_out, non_blocking=True)
+                graph.step(io=sel)
+                return
+            graph.q.copy_(q[sel])
+            graph.k_new.copy_(kn[sel])
+            graph.v_new.copy_(vn[sel])
+            graph.step()
             return
         manager.allocate_decode_step(seqs, sync=False)
         if e2e:

@@ -14,6 +14,12 @@ slack (the score rows are sized for it), and is recaptured automatically
 when the headroom is used up or the block tables were reallocated.
 Device-side conditions (PreemptionNeeded, AllocationOrderError, ...) land in
 the status word as usual; check them with DeviceContext.raise_status().
+
+Host I/O (`host_io`): for callers whose per-step inputs live in pinned host
+memory, each host buffer set gets its own captured graph in which layer m's
+Q/K/V upload (a copy stream, in layer order) and layer m's output download
+(a second copy stream, right after layer m) overlap the other layers'
+attention, instead of bracketing the whole step.
 """
 
 from __future__ import annotations
@@ -39,7 +45,7 @@ class DecodeStepGraph:
 
     def __init__(self, cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
                  seq_ids, cfg: AttentionConfig, metric_mode: int = 2, fresh: bool = True, headroom: int = 256,
-                 buffers: dict | None = None, metric_overlap: bool = True):
+                 buffers: dict | None = None, metric_overlap: bool = True, host_io: list | None = None):
         self.cache, self.tables, self.manager, self.store = cache, tables, manager, store
         self.seq_ids = list(seq_ids)
         self.cfg = cfg
@@ -64,7 +70,15 @@ class DecodeStepGraph:
         self.alloc_order = sorted(range(B), key=lambda i: self.seq_ids[i])  # reference order: sorted(seq)
         self.rows_sorted_t = torch.tensor([self.rows[i] for i in self.alloc_order], dtype=torch.int32, device=dev)
         self.counts = torch.zeros(B, dtype=torch.int32, device=dev)
+        # pinned host buffer sets {q, k_new, v_new, out} shaped like the device ones
+        self.host_io = list(host_io or [])
+        for h in self.host_io:
+            for name in ("q", "k_new", "v_new", "out"):
+                x, ref = h[name], getattr(self, name)
+                if x.shape != ref.shape or x.dtype != ref.dtype or x.is_cuda or not x.is_pinned():
+                    raise ValueError(f"host_io {name}: need a pinned host tensor {tuple(ref.shape)} {ref.dtype}")
         self.graph = None
+        self.graphs: dict = {}  # None: device buffers; i: host_io[i]
         self.replays = 0
 
     # -- capture ------------------------------------------------------------------
@@ -73,7 +87,10 @@ class DecodeStepGraph:
         t = self.tables
         return max(t.ctx_bound[r] for r in self.rows)
 
-    def _capture(self) -> None:
+    def _prepare(self) -> None:
+        """Workspaces, queue and per-layer argument structs shared by the
+        captured graphs (rebuilt when the tables are reallocated or the
+        context headroom runs out)."""
         t, dev = self.tables, self.device
         B, l, H = len(self.rows), t.num_layers, t.num_kv_heads
         self.cap_ctx = self._bounds() + self.headroom
@@ -118,13 +135,44 @@ class DecodeStepGraph:
             a.metric_stream = self.side.cuda_stream if self.side is not None else None
             args.append(a)
         self._keep = (pools, args)
+        self.graphs = {}
+        self.captured_at = self._bounds()
+
+    def _capture(self, key=None) -> None:
+        dev = self.device
+        if not self._valid_prep():
+            self._prepare()
+        pools, args = self._keep
+        p = pools[0]
+        lib = _lib.lib()
+        B = len(self.rows)
+        h = self.host_io[key] if key is not None else None
+        if h is not None:
+            self.io_in = getattr(self, "io_in", None) or torch.cuda.Stream(dev)
+            self.io_out = getattr(self, "io_out", None) or torch.cuda.Stream(dev)
 
         def body(s):
             stream = s.cuda_stream
+            ev_in = []
+            if h is not None:  # every layer's upload, in layer order, beside the step
+                fork = torch.cuda.Event()
+                fork.record(s)
+                self.io_in.wait_event(fork)
+                self.io_out.wait_event(fork)
+                with torch.cuda.stream(self.io_in):
+                    for m in range(len(args)):
+                        self.q[m].copy_(h["q"][m], non_blocking=True)
+                        self.k_new[m].copy_(h["k_new"][m], non_blocking=True)
+                        self.v_new[m].copy_(h["v_new"][m], non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(self.io_in)
+                        ev_in.append(ev)
             _lib.check(lib.kvc_alloc_decode(ctypes.byref(p), self.rows_sorted_t.data_ptr(), B, self.counts.data_ptr(),
                                             stream), "alloc_decode")
             done = []
             for m, a in enumerate(args):
+                if h is not None:
+                    s.wait_event(ev_in[m])
                 if self.side is not None and m >= 2:
                     s.wait_event(done[m - 2])  # layer m reuses layer m-2's workspace
                 _lib.check(lib.kvc_paged_decode(ctypes.byref(pools[m % len(pools)]), ctypes.byref(a), stream),
@@ -133,39 +181,64 @@ class DecodeStepGraph:
                     ev = torch.cuda.Event()
                     ev.record(self.side)
                     done.append(ev)
+                if h is not None:  # layer m's output goes down while the next layers run
+                    ev = torch.cuda.Event()
+                    ev.record(s)
+                    self.io_out.wait_event(ev)
+                    with torch.cuda.stream(self.io_out):
+                        h["out"][m].copy_(self.out[m], non_blocking=True)
             for ev in done[-2:]:  # join the side branch before the fresh clear
+                s.wait_event(ev)
+            if h is not None:
+                ev = torch.cuda.Event()
+                ev.record(self.io_out)
                 s.wait_event(ev)
             _lib.check(lib.kvc_clear_fresh(ctypes.byref(p), self.rows_t.data_ptr(), B, stream), "clear_fresh")
 
-        self.graph = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
-            with torch.cuda.graph(self.graph, stream=s):
+            with torch.cuda.graph(g, stream=s):
                 body(s)
         torch.cuda.current_stream(dev).wait_stream(s)
-        self.captured_at = self._bounds()
+        self.graphs[key] = g
+        self.graph = g
 
-    def _valid(self) -> bool:
-        return (self.graph is not None and self.tables.tables.data_ptr() == self.tables_ptr
+    def _valid_prep(self) -> bool:
+        return (hasattr(self, "_keep") and self.tables.tables.data_ptr() == self.tables_ptr
                 and self._bounds() + 1 <= self.cap_ctx)
 
-    def step(self) -> torch.Tensor:
+    def _valid(self) -> bool:
+        return self.graph is not None and self._valid_prep()
+
+    def step(self, io: int | None = None) -> torch.Tensor:
         """One decode step for the batch: allocation, every layer, fresh clear.
-        Asynchronous; returns the output buffer.  The first call runs the step
+        Asynchronous; returns the output buffer (``host_io[io]["out"]`` when
+        `io` selects a pinned host buffer set, whose inputs are uploaded and
+        outputs downloaded inside the step).  The first call runs the step
         eagerly (configuring every kernel outside a capture) and captures the
         graph for the following calls."""
+        h = self.host_io[io] if io is not None else None
         if self.graph is None:
+            if h is not None:
+                self.q.copy_(h["q"], non_blocking=True)
+                self.k_new.copy_(h["k_new"], non_blocking=True)
+                self.v_new.copy_(h["v_new"], non_blocking=True)
             self._eager_step()
-            self._capture()
-            return self.out
-        if not self._valid():
-            self._capture()
-        self.graph.replay()
+            if h is not None:
+                h["out"].copy_(self.out, non_blocking=True)
+            self._capture(io)
+            return self.out if h is None else h["out"]
+        if not self._valid_prep():
+            self._prepare()
+        if io not in self.graphs:
+            self._capture(io)
+        self.graphs[io].replay()
         for r in self.rows:
             self.tables.ctx_bound[r] += 1
         self.replays += 1
-        return self.out
+        return self.out if h is None else h["out"]
 
     def _eager_step(self) -> None:
         """The same step through paged_decode (kernel attributes, tensor maps)."""

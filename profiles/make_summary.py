@@ -104,6 +104,8 @@ L += ["",
       "| K1: warp-independent items, prefetched tables, 2 CTAs/SM | 46% of HBM | 73-80% |",
       "| K1: CUDA-graph decode step; batch-sized split-KV items; parallel partial merge | B=1 1.85 ms/step, B=64 6.89 | B=1 0.57, B=64 6.60 |",
       "| K1: metric on the graph's side branch; ex2.approx; rescale only when a max moved; finish split by batch | B=64 6.60 ms/step | 6.42 |",
+      "| K1: finish folds the C bump and queue reset, pre-wait loads, float4 merge | B=64 6.42 ms/step; l70b 10.0 | 6.24; 9.50 |",
+      "| K1: scores and partials stored L2 evict_last, discarded by their readers (never written back) | B=64 6.24 ms/step; l70b 9.50 | 6.02; 8.80 |",
       "| K2: persistent multi-layer kernel (TMEM slot ring across layers, one barrier per layer, branch-free ex2) | 1.39-1.48 ms/seq | 0.52 ms/seq |",
       "| K2: recompute mode at 128k | 33.5 ms/seq (two-pass fallback) | 7.7 ms/seq |",
       "| K4: 512-thread compaction CTAs, aggregated free-tile atomics, batched metadata moves | K3+K4 0.48 ms | 0.38 ms |",
@@ -112,7 +114,9 @@ L += ["",
       f"| KVC-full: 8 epilogue warps, chunk-max softmax, pre-multiplied normalisers, 2 CTAs/SM | 16.8 ms/layer (32k) | {f32['ms_per_layer']:.1f} |",
       "\nExperiments that were measured and dropped:",
       "* K1: eager side-stream metric (broke the PDL chain); L2 prefetch ahead of the ring (slower at every",
-      "  distance); tail-split items; smaller items at large B; packed score stores.",
+      "  distance); tail-split items; smaller items at large B (8-block items: l8b 9.9k vs 10.6k tok/s, after the",
+      "  L2-resident partials); packed score stores; a producer warp per CTA that pre-fetches each warp's next",
+      "  item and query rows into shared memory (l8b 10.5k, l70b 7.07k, m7b 18.3k vs 10.6k / 7.27k / 19.5k).",
       "* K2:",
       "  * pipelined metric pass;",
       "  * L2 prefetch ahead of the ring;",

@@ -19,8 +19,9 @@ import paper_2410_00161_b200 as K  # noqa: E402
 from paper_2410_00161_b200 import _lib  # noqa: E402
 
 
+@pytest.mark.parametrize("host", [False, True])
 @pytest.mark.parametrize("seqs,max_len,headroom", [([3, 1, 7], 300, 4), ([0, 2, 5, 9], 1200, 64)])
-def test_graph_step_equals_eager(seqs, max_len, headroom):
+def test_graph_step_equals_eager(seqs, max_len, headroom, host):
     b, d, layers, heads, r = 16, 128, 2, 4, 4
     rng = np.random.default_rng(len(seqs) * 100 + max_len)
     nblocks = 3 * layers * heads * len(seqs) * (max_len // b + 12) + 64
@@ -30,16 +31,30 @@ def test_graph_step_equals_eager(seqs, max_len, headroom):
         rig.load(st)
     cfg = K.AttentionConfig(heads * r, heads, d, layers)
     dev = rigs[0].cache.device
-    g = K.DecodeStepGraph(rigs[0].cache, rigs[0].tables, rigs[0].manager, rigs[0].store, seqs, cfg,
-                          headroom=headroom)
     B, n_q = len(seqs), heads * r
+    host_io = None
+    if host:  # two pinned host sets, used alternately (per-layer upload/download inside the step)
+        host_io = [{"q": torch.empty((layers, B, n_q, d), dtype=torch.bfloat16).pin_memory(),
+                    "k_new": torch.empty((layers, B, heads, d), dtype=torch.bfloat16).pin_memory(),
+                    "v_new": torch.empty((layers, B, heads, d), dtype=torch.bfloat16).pin_memory(),
+                    "out": torch.empty((layers, B, n_q, d), dtype=torch.bfloat16).pin_memory()} for _ in range(2)]
+    g = K.DecodeStepGraph(rigs[0].cache, rigs[0].tables, rigs[0].manager, rigs[0].store, seqs, cfg,
+                          headroom=headroom, host_io=host_io)
     steps = 2 * headroom + 3  # crosses at least one recapture
     for step in range(steps):
         q = torch.randn((layers, B, n_q, d), device=dev).to(torch.bfloat16)
         kn = torch.randn((layers, B, heads, d), device=dev).to(torch.bfloat16)
         vn = torch.randn((layers, B, heads, d), device=dev).to(torch.bfloat16)
-        g.q.copy_(q), g.k_new.copy_(kn), g.v_new.copy_(vn)
-        out_g = g.step().clone()
+        if host:
+            h = host_io[step % 2]
+            torch.cuda.synchronize()  # the set's previous step has finished with it
+            h["q"].copy_(q), h["k_new"].copy_(kn), h["v_new"].copy_(vn)
+            g.step(io=step % 2)
+            torch.cuda.synchronize()
+            out_g = h["out"].to(dev)
+        else:
+            g.q.copy_(q), g.k_new.copy_(kn), g.v_new.copy_(vn)
+            out_g = g.step().clone()
         e = rigs[1]
         e.manager.allocate_decode_step(seqs, sync=False)
         out_e = torch.empty_like(out_g)
