@@ -116,7 +116,10 @@ L += ["",
       "* K1: eager side-stream metric (broke the PDL chain); L2 prefetch ahead of the ring (slower at every",
       "  distance); tail-split items; smaller items at large B (8-block items: l8b 9.9k vs 10.6k tok/s, after the",
       "  L2-resident partials); packed score stores; a producer warp per CTA that pre-fetches each warp's next",
-      "  item and query rows into shared memory (l8b 10.5k, l70b 7.07k, m7b 18.3k vs 10.6k / 7.27k / 19.5k).",
+      "  item and query rows into shared memory (l8b 10.5k, l70b 7.07k, m7b 18.3k vs 10.6k / 7.27k / 19.5k);",
+      "  each head's last chunk as four quarter items queued last (l8b 10.4k vs 10.7k, m7b 18.1k vs 19.4k): while",
+      "  the queue drains, the warps still streaming keep HBM saturated, so the warps' end-time spread costs less",
+      "  than the extra items do.",
       "* K2:",
       "  * pipelined metric pass;",
       "  * L2 prefetch ahead of the ring;",
