@@ -30,8 +30,10 @@ cfg = subprocess.run(["python", os.path.join(HERE, "..", "tools", "summarize_con
 k1tr = sum(x["dram_read_B"] + x["dram_write_B"] for x in n["k1"])
 f32 = [x for x in fm if x["L"] == 32768][0]
 L = ["# Round 1 — measurements on B200 (one GPU)\n",
-     "All numbers come from `gpurun` calls on one B200: 148 SMs, 1965 MHz max SM clock, and no throttle",
-     "reasons in the clock samples. The roofline denominator is the HBM copy bandwidth the driver measured,",
+     "All numbers come from `gpurun` calls on one B200: 148 SMs, 1965 MHz max SM clock. The default line's",
+     f"clock samples: median {b['clocks']['sm_mhz']:.0f} MHz under load, throttle reasons "
+     f"{', '.join(b['clocks']['reasons']) or 'none'} (no hw/thermal slowdown).",
+     "The roofline denominator is the HBM copy bandwidth the driver measured,",
      f"{peak} GB/s (`MEASURED_PEAKS.json`). A read-only stream reaches more on this part: 6.8 TB/s with",
      "LDG.128 and 7.3 TB/s with TMA (`tools/microbench/readbw.cu`, table below).",
      "Regenerate with `python profiles/make_summary.py`.\n",
