@@ -303,14 +303,31 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
         }
         __syncwarp();
       }
-      float sc[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t kbase = smem_u32(kb);
+      // the block's K and V fragments go to registers first and the stage
+      // returns to the ring before the math, so the next TMA overlaps it
+      // (d <= 128: at d = 256 the fragments would not fit in registers)
+      constexpr bool kEarly = D <= 128;
+      constexpr int kVF = kEarly ? kKS : 1;
+      uint32_t kf[kKS][4], vf[kVF][4];
+      const uint32_t kbase = smem_u32(kb), vbase = smem_u32(vb);
 #pragma unroll
-      for (int kk = 0; kk < kKS; ++kk) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(kbase + swz(lm_tok, 2 * kk + lm_cadd), a0, a1, a2, a3);
-        mma16816(sc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+      for (int kk = 0; kk < kKS; ++kk)
+        ldsm_x4(kbase + swz(lm_tok, 2 * kk + lm_cadd), kf[kk][0], kf[kk][1], kf[kk][2], kf[kk][3]);
+      if constexpr (kEarly) {
+#pragma unroll
+        for (int mt = 0; mt < kKS; ++mt)
+          ldsm_x4_t(vbase + swz(lt_tok, 2 * mt + lt_cadd), vf[mt][0], vf[mt][1], vf[mt][2], vf[mt][3]);
+        __syncwarp();
+        ++done;
+        if (lane == 0) try_issue();
       }
+      // two independent accumulation chains over d
+      float sc[4] = {0.f, 0.f, 0.f, 0.f}, sc2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < kKS; ++kk)
+        mma16816((kk & 1) ? sc2 : sc, kf[kk][0], kf[kk][1], kf[kk][2], kf[kk][3], qb[kk][0], qb[kk][1]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sc[i] += sc2[i];
       const bool tv0 = g < valid, tv1 = g + 8 < valid;
       const float s00 = (tv0 && hv0) ? sc[0] * P.scale : -INFINITY;
       const float s01 = (tv0 && hv1) ? sc[1] * P.scale : -INFINITY;
@@ -346,7 +363,6 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       l1 = l1 * al1 + p01 + p11;
       const uint32_t pb0 = movmatrix_t(pack_bf16(p00, p01));
       const uint32_t pb1 = movmatrix_t(pack_bf16(p10, p11));
-      const uint32_t vbase = smem_u32(vb);
       if (rescale) {
 #pragma unroll
         for (int mt = 0; mt < kKS; ++mt) {
@@ -356,15 +372,20 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
           oacc[mt][3] *= al1;
         }
       }
+      if constexpr (kEarly) {
 #pragma unroll
-      for (int mt = 0; mt < kKS; ++mt) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(vbase + swz(lt_tok, 2 * mt + lt_cadd), a0, a1, a2, a3);
-        mma16816(oacc[mt], a0, a1, a2, a3, pb0, pb1);
+        for (int mt = 0; mt < kKS; ++mt) mma16816(oacc[mt], vf[mt][0], vf[mt][1], vf[mt][2], vf[mt][3], pb0, pb1);
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < kKS; ++mt) {
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(vbase + swz(lt_tok, 2 * mt + lt_cadd), a0, a1, a2, a3);
+          mma16816(oacc[mt], a0, a1, a2, a3, pb0, pb1);
+        }
+        __syncwarp();
+        ++done;
+        if (lane == 0) try_issue();
       }
-      __syncwarp();
-      ++done;
-      if (lane == 0) try_issue();
     }
     // ---- this item's partial (m, l, O) straight from registers ----
 #pragma unroll
