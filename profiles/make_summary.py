@@ -108,6 +108,7 @@ L += ["",
       "| K1: metric on the graph's side branch; ex2.approx; rescale only when a max moved; finish split by batch | B=64 6.60 ms/step | 6.42 |",
       "| K1: finish folds the C bump and queue reset, pre-wait loads, float4 merge | B=64 6.42 ms/step; l70b 10.0 | 6.24; 9.50 |",
       "| K1: scores and partials stored L2 evict_last, discarded by their readers (never written back) | B=64 6.24 ms/step; l70b 9.50 | 6.02; 8.80 |",
+      "| e2e: per-layer host upload/download inside the graph (`host_io`), uploads awaited per doubling layer group | e2e 9.1k tok/s | 10.6k |",
       "| K2: persistent multi-layer kernel (TMEM slot ring across layers, one barrier per layer, branch-free ex2) | 1.39-1.48 ms/seq | 0.52 ms/seq |",
       "| K2: recompute mode at 128k | 33.5 ms/seq (two-pass fallback) | 7.7 ms/seq |",
       "| K4: 512-thread compaction CTAs, aggregated free-tile atomics, batched metadata moves | K3+K4 0.48 ms | 0.38 ms |",
