@@ -347,10 +347,26 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   const int lane = threadIdx.x & 31;
   int32_t lt = 0, le = 0;
   if (!cand) {
-    for (int64_t pos = threadIdx.x; pos < n; pos += NT) {
-      const uint32_t k = keys[pos];
-      lt += k < T;
-      le += k <= T;
+    // batches of 8 uint4 per thread in flight
+    constexpr int U = 8;
+    for (int64_t base = 0; base < n; base += 4 * NT * U) {
+      uint4 k4[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);  // max_slots is a multiple of 4
+        k4[u] = pos < n ? *reinterpret_cast<const uint4 *>(keys + pos) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);
+        const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool in = pos + e < n;
+          lt += (in && kv[e] < T) ? 1 : 0;
+          le += (in && kv[e] <= T) ? 1 : 0;
+        }
+      }
     }
   } else {
     // short heads (n <= 8192): all of the head's keys in flight at once, 4
@@ -1188,7 +1204,7 @@ __device__ void warp_sort(unsigned long long *a, int cnt, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kWC * 32) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
+__global__ void __launch_bounds__(kWC * 32, 4) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
                                                           MoveArgs M, int64_t T_heads) {
   __shared__ WarpArea area[kWC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
