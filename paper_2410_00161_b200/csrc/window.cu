@@ -410,10 +410,11 @@ __device__ __forceinline__ void warp_lse_scatter32(float *m, float *z, int lane)
 __device__ __forceinline__ void epi_head_barrier(int *cnt, int target, bool leader) {
   named_sync(1, 32 * kPEW);
   if (leader) {
-    __threadfence();
-    atomicAdd(cnt, 1);
+    // release/acquire instead of two fence.sc: the named barrier orders the
+    // other epilogue threads' partial/raw writes before this release, and the
+    // acquire poll (with the named barrier after it) orders their reads after
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
     while (ld_acquire_gpu(cnt) < target) __nanosleep(32);
-    __threadfence();
   }
   named_sync(1, 32 * kPEW);
 }

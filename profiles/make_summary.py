@@ -111,6 +111,7 @@ L += ["",
       "| e2e: per-layer host upload/download inside the graph (`host_io`), uploads awaited per doubling layer group | e2e 9.1k tok/s | 10.6k |",
       "| K2: persistent multi-layer kernel (TMEM slot ring across layers, one barrier per layer, branch-free ex2) | 1.39-1.48 ms/seq | 0.52 ms/seq |",
       "| K2: recompute mode at 128k | 33.5 ms/seq (two-pass fallback) | 7.7 ms/seq |",
+      "| K2: head barrier as red.release + ld.acquire poll instead of two fence.sc (its top stall in ncu) | 0.52 ms/seq | 0.48 ms/seq |",
       "| K4: 512-thread compaction CTAs, aggregated free-tile atomics, batched metadata moves | K3+K4 0.48 ms | 0.38 ms |",
       "| prompt scatter: warp-per-block, multi-layer kernel | 2.9 ms/seq | 1.37 ms/seq |",
       "| fused prefill + compress (survivors written once) | 2.30 ms/seq | 1.15 ms/seq |",
