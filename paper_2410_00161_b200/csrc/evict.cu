@@ -178,13 +178,13 @@ __device__ __forceinline__ bool last_of_sequence(EvictState &S, int si) {
   __shared__ int last_s;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const int prev = atomicAdd(&S.done[si], 1);
+    // acq_rel arrival: releases this CTA's contributions (ordered before it
+    // by the CTA barrier), and the last arrival acquires everyone else's
+    // (read through L2 by find_digit)
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(&S.done[si]) : "memory");
     last_s = prev == S.hp - 1;
-    if (last_s) {
-      S.done[si] = 0;
-      __threadfence();
-    }
+    if (last_s) S.done[si] = 0;
   }
   __syncthreads();
   return last_s != 0;
