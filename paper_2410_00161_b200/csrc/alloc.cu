@@ -154,9 +154,15 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t *counts, int
 }
 
 // Decode demand: heads (row order given, then layer-major) with C % b == 0.
+// One CTA: head i (row-major over the batch rows, then layer x head) needs a
+// block iff its C is a multiple of the block size; its rank is the
+// exclusive count of needing heads before it (the reference's order).  Each
+// thread takes 16 consecutive heads (16 independent C loads in flight), one
+// block scan per 16K-head tile.
 __global__ void __launch_bounds__(1024) k_decode_demand(kvc_pool p, const int32_t *rows, int n_rows,
                                                        int32_t *head_rank, int32_t *out_counts,
                                                        int64_t *demand) {
+  constexpr int kPer = 16;
   using Scan = cub::BlockScan<int32_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int32_t carry;
@@ -165,23 +171,42 @@ __global__ void __launch_bounds__(1024) k_decode_demand(kvc_pool p, const int32_
   if (threadIdx.x == 0) carry = 0;
   for (int i = threadIdx.x; i < n_rows; i += blockDim.x) out_counts[i] = 0;
   __syncthreads();
-  for (int64_t base = 0; base < total_heads; base += 1024) {
-    int64_t i = base + threadIdx.x;
-    int32_t need = 0;
-    int rix = 0;
-    if (i < total_heads) {
-      rix = (int)(i / heads);
-      int64_t hidx = (int64_t)rows[rix] * heads + (i % heads);
-      need = (p.ctx[hidx] % p.block_size) == 0 ? 1 : 0;
+  for (int64_t base = 0; base < total_heads; base += 1024 * kPer) {
+    const int64_t i0 = base + (int64_t)threadIdx.x * kPer;
+    uint32_t needm = 0;  // bit j: head i0 + j needs a block
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t i = i0 + j;
+      if (i < total_heads) {
+        const int rix = (int)(i / heads);
+        const int64_t hidx = (int64_t)rows[rix] * heads + (i % heads);
+        needm |= ((p.ctx[hidx] % p.block_size) == 0 ? 1u : 0u) << j;
+      }
     }
     int32_t excl, total;
-    Scan(tmp).ExclusiveSum(need, excl, total);
-    if (i < total_heads) {
-      head_rank[i] = need ? carry + excl : -1;
-      if (need) atomicAdd(&out_counts[rix], 1);
+    Scan(tmp).ExclusiveSum(__popc(needm), excl, total);
+    const int32_t c0 = carry;
+    int32_t rank = c0 + excl;
+    int cur_r = -1, cur_n = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t i = i0 + j;
+      if (i < total_heads) {
+        const bool need = (needm >> j) & 1u;
+        head_rank[i] = need ? rank : -1;
+        rank += need ? 1 : 0;
+        const int rix = (int)(i / heads);
+        if (rix != cur_r) {
+          if (cur_n) atomicAdd(&out_counts[cur_r], cur_n);
+          cur_r = rix;
+          cur_n = 0;
+        }
+        cur_n += need ? 1 : 0;
+      }
     }
+    if (cur_n) atomicAdd(&out_counts[cur_r], cur_n);
     __syncthreads();
-    if (threadIdx.x == 0) carry += total;
+    if (threadIdx.x == 0) carry = c0 + total;
     __syncthreads();
   }
   if (threadIdx.x == 0) *demand = carry;
