@@ -696,7 +696,8 @@ def main():
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (unit-normal Q/K/V, random-init shapes; no checkpoints)", "config": config_dict(args, world),
         "hbm_gbs_decode_step": dec["bytes_per_step"] / (step_ms * 1e-3) / 1e9,
-        "roofline": {"bound": "hbm", "kernel": "k_paged_decode (K1, one launch per layer)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "K1 per layer: k_decode_stream + k_decode_finish (+ k_decode_metric, graph side branch)",
                      "achieved": dec["k1_gbs"], "peak": peak, "unit": "GB/s", "frac": dec["k1_gbs"] / peak,
                      "peak_source": peak_kind, "traffic": k1_traffic(),
                      "bytes_per_launch": dec["k1_bytes_mean"], "launch_ms": dec["k1_ms_mean"],
