@@ -108,6 +108,7 @@ L += ["",
       "| K1: metric on the graph's side branch; ex2.approx; rescale only when a max moved; finish split by batch | B=64 6.60 ms/step | 6.42 |",
       "| K1: finish folds the C bump and queue reset, pre-wait loads, float4 merge | B=64 6.42 ms/step; l70b 10.0 | 6.24; 9.50 |",
       "| K1: scores and partials stored L2 evict_last, discarded by their readers (never written back) | B=64 6.24 ms/step; l70b 9.50 | 6.02; 8.80 |",
+      "| K0: k_decode_demand with 16 heads per thread (independent C loads, one scan per tile) | 26 us/step | 19 us/step |",
       "| e2e: per-layer host upload/download inside the graph (`host_io`), uploads awaited per doubling layer group | e2e 9.1k tok/s | 10.6k |",
       "| K2: persistent multi-layer kernel (TMEM slot ring across layers, one barrier per layer, branch-free ex2) | 1.39-1.48 ms/seq | 0.52 ms/seq |",
       "| K2: recompute mode at 128k | 33.5 ms/seq (two-pass fallback) | 7.7 ms/seq |",
@@ -132,5 +133,12 @@ L += ["",
       "  * split head barrier with the previous layer's install between arrive and wait (0.635 vs 0.52 ms/seq).",
       "* K4: PDL-overlapped K/V copy; the copy inside the compaction warps; unrolled and warp-aggregated or",
       "  privatised histogram atomics in the selects; pipelined survivor pass.",
-      "* KVC-full: 30% of the exp2s as an FMA polynomial. The epilogue is issue-bound, so it was slower."]
+      "* KVC-full: 30% of the exp2s as an FMA polynomial. The epilogue is issue-bound, so it was slower.",
+      "* K2: spinning without `nanosleep` in the head barrier poll (0.479 vs 0.478 ms/seq).",
+      "* K3: 8 uint4 key loads in flight in `k_hist` (60 registers halved its occupancy; decode round 1.16 vs",
+      "  1.06 ms); kept in `k_bounds`' long-head path, where registers went down.",
+      "",
+      "Next for K4: `k_compact16` spends 46 of its ~110 us per head in the per-head threshold and tie-cut",
+      "selects (`KVC_K4_TRACE=1`). At 8x the per-head threshold lies among the <=16 largest keys below the",
+      "sequence threshold T*, so a one-pass candidate capture in `k_bounds` could replace most of the radix passes."]
 open(os.path.join(HERE, "r1_summary.md"), "w").write("\n".join(L) + "\n")
