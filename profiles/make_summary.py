@@ -135,6 +135,13 @@ L += ["",
       "  privatised histogram atomics in the selects; pipelined survivor pass.",
       "* KVC-full: 30% of the exp2s as an FMA polynomial. The epilogue is issue-bound, so it was slower.",
       "* K2: spinning without `nanosleep` in the head barrier poll (0.479 vs 0.478 ms/seq).",
+      "* K1: 8-byte packed score stores (full sectors) with the L2-resident scores: l8b +0.3%, l70b -0.7%,",
+      "  m7b -0.5%.",
+      "",
+      "Where the decode metric's 5.5% goes (ncu `--graph-profiling graph`, one whole step): it adds only",
+      "0.81 GB of DRAM traffic per step. That is the 16.8 MB/layer metric read-modify-write plus ~8 MB/layer",
+      "of score lines that leave L2, so the 33.5 MB/layer score rows mostly stay in L2. The time goes to the",
+      "score stores themselves: with the metric off, forcing the stores costs 0.29 ms of the 0.39 ms.",
       "* K3: 8 uint4 key loads in flight in `k_hist` (60 registers halved its occupancy; decode round 1.16 vs",
       "  1.06 ms); kept in `k_bounds`' long-head path, where registers went down.",
       "",
