@@ -136,7 +136,8 @@ L += ["",
       "* KVC-full: 30% of the exp2s as an FMA polynomial. The epilogue is issue-bound, so it was slower.",
       "* K2: spinning without `nanosleep` in the head barrier poll (0.479 vs 0.478 ms/seq).",
       "* K1: 8-byte packed score stores (full sectors) with the L2-resident scores: l8b +0.3%, l70b -0.7%,",
-      "  m7b -0.5%.",
+      "  m7b -0.5%; per-block score staging in shared memory written by one `cp.async.bulk` store (l8b 10.5k vs",
+      "  10.7k: the per-block proxy fence and bulk-group wait cost more than the four stores).",
       "",
       "Where the decode metric's 5.5% goes (ncu `--graph-profiling graph`, one whole step): it adds only",
       "0.81 GB of DRAM traffic per step. That is the 16.8 MB/layer metric read-modify-write plus ~8 MB/layer",
