@@ -205,7 +205,7 @@ def _scratch_bytes(plan: EvictionPlan, hp: int) -> int:
     n = len(plan.seq_ids)
     T = n * hp
     # keys + per-head counters + per-sequence digit histograms + candidate lists (short heads)
-    return T * ((plan.max_slots + 3) // 4 * 4) * 4 + T * 20 + n * (2048 * 4 + 40) + T * 2 * 256 * 8 + (1 << 16)
+    return T * ((plan.max_slots + 3) // 4 * 4) * 4 + T * 28 + n * (2048 * 4 + 40) + T * 2 * 256 * 8 + (1 << 16)
 
 
 def schedule_evictions(tables: BlockTables, store: MetricsStore, budgets: Mapping[int, int],

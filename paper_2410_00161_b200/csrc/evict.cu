@@ -47,6 +47,7 @@ struct EvictState {
   int32_t *hi;        // [T] U_h
   int32_t *ltc;       // [T] keys < T*
   int32_t *lec;       // [T] keys <= T*
+  int32_t *lt1, *lt2; // [T] keys < T* sharing T*'s top 11 / top 22 bits (select shortcuts)
   // per sequence
   int32_t *R;         // [n_seqs][kBins] contribution deltas per digit
   int32_t *done;      // [n_seqs] heads finished in the current histogram kernel (last one finds the digit)
@@ -345,7 +346,8 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   if (threadIdx.x < 2) cnt_s[threadIdx.x] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  int32_t lt = 0, le = 0;
+  int32_t lt = 0, le = 0, l1 = 0, l2 = 0;
+  const uint32_t T1 = T >> 21, T2 = T >> 10;
   if (!cand) {
     // batches of 8 uint4 per thread in flight
     constexpr int U = 8;
@@ -363,8 +365,11 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const bool in = pos + e < n;
-          lt += (in && kv[e] < T) ? 1 : 0;
+          const bool below = in && kv[e] < T;
+          lt += below ? 1 : 0;
           le += (in && kv[e] <= T) ? 1 : 0;
+          l1 += (below && (kv[e] >> 21) == T1) ? 1 : 0;
+          l2 += (below && (kv[e] >> 10) == T2) ? 1 : 0;
         }
       }
     }
@@ -387,8 +392,11 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const bool in = pos0 + i < n;
-        mlt |= (in && kv[i] < T ? 1u : 0u) << (u * 4 + i);
+        const bool below = in && kv[i] < T;
+        mlt |= (below ? 1u : 0u) << (u * 4 + i);
         meq |= (in && kv[i] == T ? 1u : 0u) << (u * 4 + i);
+        l1 += (below && (kv[i] >> 21) == T1) ? 1 : 0;
+        l2 += (below && (kv[i] >> 10) == T2) ? 1 : 0;
       }
     }
     using Scan = cub::BlockScan<int32_t, NT>;
@@ -419,7 +427,13 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   lt = Red(tmp).Sum(lt);
   __syncthreads();
   le = Red(tmp).Sum(le);
+  __syncthreads();
+  l1 = Red(tmp).Sum(l1);
+  __syncthreads();
+  l2 = Red(tmp).Sum(l2);
   if (threadIdx.x == 0) {
+    S.lt1[g] = l1;
+    S.lt2[g] = l2;
     const int cap = S.cap[g];
     S.lo[g] = lt / b < cap ? lt / b : cap;
     S.hi[g] = le / b < cap ? le / b : cap;
@@ -761,14 +775,14 @@ __device__ void scan_hist16(int32_t *hist) {  // inclusive, NT threads
 // many valid positions hold it.
 template <int NT, typename Get4>
 __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, int64_t *rank_out,
-                             int64_t *eq_out) {
+                             int64_t *eq_out, int lv0 = 0, uint32_t pre0 = 0) {
   __shared__ uint32_t pre_s;
   __shared__ int64_t rank_s, eq_s;
   const int shifts[3] = {21, 10, 0};
   const int bitsv[3] = {11, 11, 10};
-  uint32_t pre = 0;
+  uint32_t pre = pre0;  // the digits above level lv0, when known
   int64_t eq = 0;
-  for (int lv = 0; lv < 3; ++lv) {
+  for (int lv = lv0; lv < 3; ++lv) {
     const int shift = shifts[lv], bits = bitsv[lv];
     const int shift_hi = shift + bits;
     const uint32_t dmask = (1u << bits) - 1;
@@ -838,12 +852,24 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
     tie_rank = target - lt;
     tie_cnt = le - lt;
   } else {
-    T = select16<NT>(hist, n, target, [&](int64_t pos, uint32_t *v, bool *ok) {
+    // The keys < T* that share T*'s top 22 (11) bits are exactly the largest
+    // lt2 (lt1) keys below T*: when the target is among them the select
+    // starts at level 3 (2) with that prefix (one or two passes fewer).
+    const int64_t from_top = lt - 1 - target;
+    int lv0 = 0;
+    uint32_t pre0 = 0;
+    int64_t rank0 = target;
+    if (S.lt2[g] > from_top) {
+      lv0 = 2; pre0 = Tstar >> 10; rank0 = S.lt2[g] - 1 - from_top;
+    } else if (S.lt1[g] > from_top) {
+      lv0 = 1; pre0 = Tstar >> 21; rank0 = S.lt1[g] - 1 - from_top;
+    }
+    T = select16<NT>(hist, n, rank0, [&](int64_t pos, uint32_t *v, bool *ok) {
       const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
       v[0] = k4.x; v[1] = k4.y; v[2] = k4.z; v[3] = k4.w;
 #pragma unroll
       for (int i = 0; i < 4; ++i) ok[i] = pos + i < n && v[i] < Tstar;
-    }, &tie_rank, &tie_cnt);
+    }, &tie_rank, &tie_cnt, lv0, pre0);
   }
   if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 1] = t_; }
   // ---- tie cut: ties at T ordered by (occupied, logical, position) ----
@@ -1745,6 +1771,8 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.hi = sc.take<int32_t>(T);
   S.ltc = sc.take<int32_t>(T);
   S.lec = sc.take<int32_t>(T);
+  S.lt1 = sc.take<int32_t>(T);
+  S.lt2 = sc.take<int32_t>(T);
   S.R = sc.take<int32_t>((int64_t)a->n_seqs * kBins);
   S.done = sc.take<int32_t>(a->n_seqs);
   S.prefix = sc.take<uint32_t>(a->n_seqs);
@@ -1752,7 +1780,7 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.seq_moves = sc.take<int64_t>(a->n_seqs);
   // candidate lists for the warp-per-head compaction of short heads
   S.cand = small_heads(S) && pool->block_size == 16 ? sc.take<unsigned long long>(T * 2 * kCand) : nullptr;
-  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.R || !S.done || !S.prefix || !S.E || !S.seq_moves ||
+  if (!S.keys || !S.cap || !S.lo || !S.hi || !S.ltc || !S.lec || !S.lt1 || !S.lt2 || !S.R || !S.done || !S.prefix || !S.E || !S.seq_moves ||
       (small_heads(S) && pool->block_size == 16 && !S.cand))
     return KVC_ERR_INVALID;
   return KVC_OK;
