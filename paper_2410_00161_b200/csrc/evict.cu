@@ -877,7 +877,49 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
     return pos < C ? (0x80000000u | (uint32_t)(lg + 1)) : (uint32_t)pos;
   };
   uint32_t Sx = 0xffffffffu;
-  if (tie_rank + 1 < tie_cnt) {
+  constexpr int kTieMax = 512;
+  if (tie_rank + 1 < tie_cnt && tie_cnt <= kTieMax) {
+    // few ties (the pooled metric repeats a local maximum over neighbouring
+    // slots): one pass collects their secondary keys (distinct: logical
+    // positions, or positions past C) into shared memory; the tie_rank-th
+    // smallest is the value with exactly tie_rank smaller ones
+    __shared__ uint32_t tie_s[kTieMax];
+    __shared__ int tie_n;
+    if (threadIdx.x == 0) tie_n = 0;
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q * 4 < n; q += NT) {
+      const int64_t pos = q * 4;  // rows padded to 4
+      const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
+      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) any |= pos + i < n && kv[i] == T;
+      if (!any) continue;
+      const int4 l4 = *reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[pos / 16] * 16 + pos % 16);
+      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (pos + i < n && kv[i] == T) {
+          const int k = atomicAdd(&tie_n, 1);
+          if (k < kTieMax) tie_s[k] = sec(pos + i, lv[i]);
+        }
+      }
+    }
+    __syncthreads();
+    const int nt = tie_n < kTieMax ? tie_n : kTieMax;
+    __shared__ uint32_t sx_s;
+    if (threadIdx.x == 0) sx_s = 0xffffffffu;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt; i += NT) {
+      const uint32_t v = tie_s[i];
+      int below = 0;
+      for (int j = 0; j < nt; ++j) below += tie_s[j] < v ? 1 : 0;
+      if (below == tie_rank) sx_s = v;
+    }
+    __syncthreads();
+    Sx = sx_s;
+    if (threadIdx.x == 0 && tie_n != tie_cnt) set_status(S.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, tie_n);
+  } else if (tie_rank + 1 < tie_cnt) {
     int64_t dummy, dummy2;
     Sx = select16<NT>(hist, n, tie_rank, [&](int64_t pos, uint32_t *v, bool *ok) {
       const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);  // pos % 4 == 0, rows padded to 4
