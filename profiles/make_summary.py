@@ -136,6 +136,8 @@ L += ["",
       "  privatised histogram atomics in the selects; pipelined survivor pass.",
       "* KVC-full: 30% of the exp2s as an FMA polynomial. The epilogue is issue-bound, so it was slower.",
       "* K2: spinning without `nanosleep` in the head barrier poll (0.479 vs 0.478 ms/seq).",
+      "* K4: the same one-pass tie cut in the warp-per-head `k_compact_warp` (decode-round compress 1.105 vs",
+      "  1.04 ms: ties are rare on that path).",
       "* K1: 8-byte packed score stores (full sectors) with the L2-resident scores: l8b +0.3%, l70b -0.7%,",
       "  m7b -0.5%; per-block score staging in shared memory written by one `cp.async.bulk` store (l8b 10.5k vs",
       "  10.7k: the per-block proxy fence and bulk-group wait cost more than the four stores).",
