@@ -300,17 +300,45 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
   if (threadIdx.x == 0) below_s = 0;
   __syncthreads();
   int32_t below = 0;
-  for (int64_t base = 0; base < n; base += 4 * NT) {
-    const int64_t pos = base + 4 * threadIdx.x;  // max_slots is a multiple of 4
-    uint4 k4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-    if (pos < n) k4 = *reinterpret_cast<const uint4 *>(keys + pos);
-    const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+  // long heads (NT = 512: one wave of CTAs, occupancy irrelevant): U uint4
+  // loads per thread in flight before the histogram updates; the decode
+  // round's short heads (NT = 256) keep one, for occupancy
+  constexpr int U = NT >= 512 ? 8 : 1;
+  if constexpr (U == 1) {
+    for (int64_t base = 0; base < n; base += 4 * NT) {
+      const int64_t pos = base + 4 * threadIdx.x;  // max_slots is a multiple of 4
+      uint4 k4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      if (pos < n) k4 = *reinterpret_cast<const uint4 *>(keys + pos);
+      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const bool in = pos + e < n;
-      const uint32_t top = kv[e] >> shift_hi;
-      below += (in && top < pre) ? 1 : 0;
-      hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
+      for (int e = 0; e < 4; ++e) {
+        const bool in = pos + e < n;
+        const uint32_t top = kv[e] >> shift_hi;
+        below += (in && top < pre) ? 1 : 0;
+        hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
+      }
+    }
+  } else {
+    for (int64_t base = 0; base < n; base += 4 * NT * U) {
+      uint4 k4[U];
+  #pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);  // max_slots is a multiple of 4
+        k4[u] = pos < n ? *reinterpret_cast<const uint4 *>(keys + pos)
+                        : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      }
+  #pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);
+        const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+  #pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool in = pos + e < n;
+          const uint32_t top = kv[e] >> shift_hi;
+          below += (in && top < pre) ? 1 : 0;
+          hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
+        }
+      }
     }
   }
   below = __reduce_add_sync(0xffffffffu, below);
@@ -395,8 +423,6 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
         const bool below = in && kv[i] < T;
         mlt |= (below ? 1u : 0u) << (u * 4 + i);
         meq |= (in && kv[i] == T ? 1u : 0u) << (u * 4 + i);
-        l1 += (below && (kv[i] >> 21) == T1) ? 1 : 0;
-        l2 += (below && (kv[i] >> 10) == T2) ? 1 : 0;
       }
     }
     using Scan = cub::BlockScan<int32_t, NT>;
@@ -427,10 +453,12 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   lt = Red(tmp).Sum(lt);
   __syncthreads();
   le = Red(tmp).Sum(le);
-  __syncthreads();
-  l1 = Red(tmp).Sum(l1);
-  __syncthreads();
-  l2 = Red(tmp).Sum(l2);
+  if (!cand) {  // top-bin counts for k_compact16's select shortcut (long heads only)
+    __syncthreads();
+    l1 = Red(tmp).Sum(l1);
+    __syncthreads();
+    l2 = Red(tmp).Sum(l2);
+  }
   if (threadIdx.x == 0) {
     S.lt1[g] = l1;
     S.lt2[g] = l2;
