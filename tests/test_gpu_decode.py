@@ -116,6 +116,11 @@ CONFIGS = [
     (4, 32, 2, 3, 90, 3),
     (2, 16, 4, 1, 50, 0),
     (16, 8, 1, 8, 100, 2),
+    # fast path with group sizes off the r in {1,2,4,8} metric kernels:
+    # generic metric pass, odd output shares per CTA
+    (16, 128, 2, 3, 900, 0),
+    (16, 64, 3, 6, 1200, 0),
+    (16, 128, 4, 1, 800, 0),
 ]
 
 
