@@ -180,7 +180,7 @@ typedef struct kvc_decode_args {
   int32_t append_fresh;     /* fresh flag for appended slots */
   int32_t max_ctx;          /* upper bound on C (+1 if appending) over the batch */
   int32_t splits;           /* 0 = auto, else CTAs (cluster size) per head */
-  int32_t *queue;           /* NULL, or a caller-owned device int32[1 + batch*heads]
+  int32_t *queue;           /* NULL, or a caller-owned device int32[2 + batch*heads]
                                that is zero on entry; the call leaves it zero, so
                                the caller allocates it once and skips a memset
                                per call.  NULL: the call zeroes a scratch copy. */

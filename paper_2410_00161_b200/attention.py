@@ -93,7 +93,7 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     need = _lib.lib().kvc_decode_scratch_bytes(ctypes.byref(p), B, cfg.num_query_heads, a.max_ctx)
     with_scratch(p, dev, need)
     stream = _lib.stream_ptr(dev)
-    a.queue = _lib.DeviceContext.get(dev).decode_queue(1 + B * tables.num_kv_heads, stream or 0).data_ptr()
+    a.queue = _lib.DeviceContext.get(dev).decode_queue(2 + B * tables.num_kv_heads, stream or 0).data_ptr()
     _lib.check(_lib.lib().kvc_paged_decode(ctypes.byref(p), ctypes.byref(a), stream), "paged_decode")
     return out
 

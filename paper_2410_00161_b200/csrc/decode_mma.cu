@@ -73,6 +73,7 @@ struct Params {
   int need_scores;  // a metric or rows pass reads the score row (else kernel A skips it)
   void *metric_stream;
   int counter_ready;
+  int early_pull;   // kernel A pulls its first item before griddepcontrol.wait (host-checked)
   float *scores;    // [pairs][max_ctx_pad][r]
   float *part_ml;   // [pairs][n_ck][2][kHP]
   float *part_o;    // [pairs][n_ck][r][D]
@@ -222,16 +223,10 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
   }
-  __syncwarp();
-  pdl_wait();     // the previous kernel's writes (ctx, tables, q, queue) are visible
-  pdl_trigger();  // let kernel B's CTAs launch and park in griddepcontrol.wait
   const uint64_t pol = policy_evict_first();
   // scores and partials are read back within the layer: keep them in L2
   // (their readers discard the lines, so they never reach HBM)
   const uint64_t pol_keep = policy_evict_last();
-  fetch_item(P, wit[0], lane);
-  fetch_item(P, wit[1], lane);
-
   // the warp's block stream: all blocks of wit[cur], then of wit[cur^1]
   int cur = 0;
   int iss_item = 0, iss_k = 0;  // next fill: block iss_k of wit[(cur+iss_item)&1]
@@ -255,6 +250,21 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
       ++iss_k;
     }
   };
+  if (P.early_pull) {
+    // First pull and its TMA loads before the dependency wait: the host
+    // allows this only when the kernel this one overlaps is the previous
+    // launch's kernel B for another layer, which writes none of what the
+    // pull reads (this launch's queue head, C, tables, rows); queries are
+    // read after the wait.
+    if (lane == 0) wit[1].id = -1;
+    fetch_item(P, wit[0], lane);
+    if (lane == 0) try_issue();
+  }
+  __syncwarp();
+  pdl_wait();     // the previous kernel's writes (ctx, tables, q, queue) are visible
+  pdl_trigger();  // let kernel B's CTAs launch and park in griddepcontrol.wait
+  if (!P.early_pull) fetch_item(P, wit[0], lane);
+  fetch_item(P, wit[1], lane);
   if (lane == 0) try_issue();
 
   const int lm_tok = (lane & 7) + ((lane >> 3) & 1) * 8;
@@ -847,7 +857,7 @@ int launch(Params &P, cudaStream_t s) {
   if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
   int grid = n_sm * per_sm;
   if (grid > P.n_items) grid = P.n_items;
-  if (!P.counter_ready) cudaMemsetAsync(P.counter, 0, (1 + P.batch * P.p.num_kv_heads) * sizeof(int), s);
+  if (!P.counter_ready) cudaMemsetAsync(P.pair_done - 2, 0, (2 + P.batch * P.p.num_kv_heads) * sizeof(int), s);
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -919,7 +929,7 @@ static int64_t kvc_decode_mma_scratch(const kvc_pool *pool, int batch, int r, in
   const int tok = item_blocks_for(pairs, max_ctx) * kBlk;
   const int64_t ctxp = ((int64_t)max_ctx + tok - 1) / tok * tok;
   const int64_t nck = ctxp / tok;
-  return (1 + pairs) * 4 + 256 + pairs * ctxp * r * 4 + pairs * nck * 2 * kHP * 4 + pairs * nck * r * pool->head_dim * 4 +
+  return (2 + pairs) * 4 + 256 + pairs * ctxp * r * 4 + pairs * nck * 2 * kHP * 4 + pairs * nck * r * pool->head_dim * 4 +
          4096;
 }
 
@@ -965,10 +975,30 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   char *base = reinterpret_cast<char *>(pool->scratch);
   // work-queue head + per-pair counters: the caller's persistent zeroed
   // array (left zero by kernel B), else a scratch copy zeroed per launch
-  P.counter = a->queue ? a->queue : reinterpret_cast<int *>(base);
-  P.pair_done = P.counter + 1;
+  // two queue heads, alternating per launch on a stream (a launch may pull
+  // from its head while the previous launch's kernel B still runs), then
+  // the per-pair counters
+  int *qbase = a->queue ? a->queue : reinterpret_cast<int *>(base);
+  int parity = 0;
+  bool early = false;
+  {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, std::pair<long long, int>> last;  // launches, last layer
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = last.find(s);
+    const long long n_prev = it == last.end() ? 0 : it->second.first;
+    const int layer_prev = it == last.end() ? -1 : it->second.second;
+    parity = (int)(n_prev & 1);
+    // the kernel A of this launch overlaps the previous launch's kernel B on
+    // this stream: safe to pull early unless that one bumped this layer's C
+    early = a->queue && layer_prev >= 0 && layer_prev != a->layer && !getenv("KVC_NO_EARLY_PULL");
+    last[s] = {n_prev + 1, a->layer};
+  }
+  P.counter = qbase + parity;
+  P.pair_done = qbase + 2;
   P.counter_ready = a->queue ? 1 : 0;
-  int64_t off = ((int64_t)(1 + a->batch * H) * 4 + 255) / 256 * 256;
+  P.early_pull = early ? 1 : 0;
+  int64_t off = ((int64_t)(2 + a->batch * H) * 4 + 255) / 256 * 256;
   P.scores = reinterpret_cast<float *>(base + off);
   off += (int64_t)a->batch * H * P.max_ctx_pad * r * 4;
   P.part_ml = reinterpret_cast<float *>(base + off);

@@ -106,7 +106,7 @@ class DecodeStepGraph:
         nws = (int(os.environ.get("KVC_GRAPH_WS", "2")) if self.metric_overlap else 1)
         self.ws = [torch.empty(max(dec_need, alloc_need) + (1 << 20), dtype=torch.uint8, device=dev)
                    for _ in range(nws)]
-        self.queue = torch.zeros(1 + B * H, dtype=torch.int32, device=dev)
+        self.queue = torch.zeros(2 + B * H, dtype=torch.int32, device=dev)
         p.scratch, p.scratch_bytes = self.ws[0].data_ptr(), self.ws[0].numel()
         pools = [p]
         for w in self.ws[1:]:
