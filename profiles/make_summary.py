@@ -108,6 +108,7 @@ L += ["",
       "| K1: metric on the graph's side branch; ex2.approx; rescale only when a max moved; finish split by batch | B=64 6.60 ms/step | 6.42 |",
       "| K1: finish folds the C bump and queue reset, pre-wait loads, float4 merge | B=64 6.42 ms/step; l70b 10.0 | 6.24; 9.50 |",
       "| K1: scores and partials stored L2 evict_last, discarded by their readers (never written back) | B=64 6.24 ms/step; l70b 9.50 | 6.02; 8.80 |",
+      "| K1: first work-item pull and TMA loads before griddepcontrol.wait (alternating queue heads) | 10.78k tok/s | 10.87k tok/s (same box) |",
       "| K0: k_decode_demand with 16 heads per thread (independent C loads, one scan per tile) | 26 us/step | 19 us/step |",
       "| e2e: per-layer host upload/download inside the graph (`host_io`), uploads awaited per doubling layer group | e2e 9.1k tok/s | 10.6k |",
       "| K2: persistent multi-layer kernel (TMEM slot ring across layers, one barrier per layer, branch-free ex2) | 1.39-1.48 ms/seq | 0.52 ms/seq |",
