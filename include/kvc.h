@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define KVC_ABI_VERSION 1
+#define KVC_ABI_VERSION 2 /* 2: kvc_decode_args.early_pull; queue int32[2 + batch*heads] */
 #define KVC_FREE_TILE 1024 /* blocks per free-count tile */
 
 typedef enum kvc_status {
@@ -189,6 +189,14 @@ typedef struct kvc_decode_args {
                                after this call's attention; the caller joins it
                                and must not reuse this call's scratch before
                                (DecodeStepGraph double-buffers). */
+  int32_t early_pull;       /* 1: the caller guarantees that the work enqueued on
+                               `stream` right before this call is a
+                               kvc_paged_decode of ANOTHER layer over the same
+                               `queue` (consecutive layers of one decode step),
+                               so this call's first work pull and its first KV
+                               loads may run before that call finishes.  0 (the
+                               safe default): everything waits for the prior
+                               stream work (allocator, compaction, scatter, ...). */
 } kvc_decode_args;
 
 int kvc_paged_decode(const kvc_pool *pool, const kvc_decode_args *args, void *stream);

@@ -342,15 +342,19 @@ def full_metric(q, k, num_kv_heads, excluded=10, aggregation="L2"):
     n_q, L, d = q.shape
     r = n_q // num_kv_heads
     out = np.zeros((num_kv_heads, L))
-    causal = np.tril(np.ones((L, L), dtype=bool))
+    # query rows in blocks (each row's causal softmax is independent), so the
+    # (r, rows, L) tensors stay small at long prompts; same arithmetic
+    rb = max(1, min(L, (1 << 22) // max(1, r * L)))
+    cols = np.arange(L)[None, :]
     for h in range(num_kv_heads):
-        s = q[h * r : (h + 1) * r] @ k[h].T / math.sqrt(d)
-        s = np.where(causal[None], s, -np.inf)
-        p = np.exp(s - s.max(axis=2, keepdims=True))
-        p /= p.sum(axis=2, keepdims=True)
-        c = agg(p, aggregation).sum(axis=0)  # (L_q, L_k)
-        keep = np.arange(L)[:, None] >= np.arange(L)[None, :] + excluded
-        out[h] = np.where(keep, c, 0.0).sum(axis=0)
+        for i0 in range(0, L, rb):
+            rows = np.arange(i0, min(L, i0 + rb))[:, None]
+            s = q[h * r : (h + 1) * r, i0 : i0 + rb] @ k[h].T / math.sqrt(d)
+            s = np.where((cols <= rows)[None], s, -np.inf)
+            p = np.exp(s - s.max(axis=2, keepdims=True))
+            p /= p.sum(axis=2, keepdims=True)
+            c = agg(p, aggregation).sum(axis=0)  # (rows, L_k)
+            out[h] += np.where(rows >= cols + excluded, c, 0.0).sum(axis=0)
     return out
 
 

@@ -54,7 +54,7 @@ class DecodeArgs(ctypes.Structure):
         ("seq_rows", _p), ("batch", _i32), ("layer", _i32), ("num_query_heads", _i32),
         ("q", _p), ("k_new", _p), ("v_new", _p), ("out", _p), ("out_f32", _i32),
         ("rows_out", _p), ("rows_stride", _i64), ("metric_mode", _i32), ("append_fresh", _i32),
-        ("max_ctx", _i32), ("splits", _i32), ("queue", _p), ("metric_stream", _p),
+        ("max_ctx", _i32), ("splits", _i32), ("queue", _p), ("metric_stream", _p), ("early_pull", _i32),
     ]
 
 

@@ -48,7 +48,7 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
                  fresh: bool = True, out: torch.Tensor | None = None, out_f32: bool = False,
                  rows_out: torch.Tensor | None = None, rows_tensor: torch.Tensor | None = None,
                  host_rows: list | None = None, max_ctx: int | None = None,
-                 splits: int = 0) -> torch.Tensor:
+                 splits: int = 0, early_pull: bool = False) -> torch.Tensor:
     """Batched single-token decode for one layer (asynchronous, no host sync).
 
     query (B, n_q, d) bf16; k_new/v_new (B, H, d) bf16 are appended at each
@@ -56,6 +56,12 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     metric_mode 1/2 adds sum_h p (L1) or p^2 (L2) to every attended slot's
     metric.  rows_out, if given, receives the (B, H, r, stride) weights.
     Returns out (B, n_q, d) bf16 (f32 with out_f32).
+
+    early_pull: the caller guarantees that the last work on the current
+    stream is this same call for another layer (consecutive layers of one
+    decode step, with rows_tensor given so nothing is enqueued in between);
+    the kernel may then start pulling work and streaming KV before that
+    launch finishes (kvc_decode_args.early_pull).
     """
     dev = cache.device
     B = query.shape[0]
@@ -70,9 +76,8 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     if max_ctx is None:
         max_ctx = max((tables.ctx_bound[r] for r in host_rows), default=1)
         max_ctx += 1 if append else 0
-    if append:
-        for r in host_rows:
-            tables.ctx_bound[r] += 1
+    if append:  # one more KV in this layer of every row (a step's l calls raise the row bound by 1)
+        tables.ctx_bound.bump(host_rows, layer)
     a = _lib.DecodeArgs()
     a.seq_rows = rows_tensor.data_ptr()
     a.batch = B
@@ -89,6 +94,7 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     a.append_fresh = int(fresh)
     a.max_ctx = max(1, int(max_ctx))
     a.splits = splits
+    a.early_pull = int(bool(early_pull))
     p = pool_struct(cache=cache, tables=tables, store=store)
     need = _lib.lib().kvc_decode_scratch_bytes(ctypes.byref(p), B, cfg.num_query_heads, a.max_ctx)
     with_scratch(p, dev, need)

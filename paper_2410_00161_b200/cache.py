@@ -63,6 +63,35 @@ class UnifiedKVCache:
         return self.values.view(self.num_blocks * self.block_size, self.head_dim)
 
 
+class CtxBound:
+    """Host upper bound on the context length of every (row, layer), so that
+    launches size their work without reading C back from the device.
+
+    ``bound[row]`` is the bound over the row's layers and ``bound[row] = v``
+    sets every layer of the row; ``bump(rows, layer)`` records one decode
+    append to one layer (one paged_decode call), ``bump_rows(rows)`` one to
+    every layer (one whole decode step), so a step of l per-layer calls
+    raises the row bound by 1, not by l."""
+
+    def __init__(self, max_seqs: int, num_layers: int):
+        self.a = np.zeros((max_seqs, max(1, num_layers)), dtype=np.int64)
+
+    def __len__(self) -> int:
+        return self.a.shape[0]
+
+    def __getitem__(self, row: int) -> int:
+        return int(self.a[row].max())
+
+    def __setitem__(self, row: int, value: int) -> None:
+        self.a[row, :] = int(value)
+
+    def bump(self, rows, layer: int) -> None:
+        self.a[np.asarray(rows, dtype=np.int64), layer] += 1
+
+    def bump_rows(self, rows) -> None:
+        self.a[np.asarray(rows, dtype=np.int64), :] += 1
+
+
 class BlockTables:
     """Device block tables + context lengths for up to ``max_seqs`` sequences."""
 
@@ -80,8 +109,8 @@ class BlockTables:
         self.ctx = torch.zeros(shape, dtype=torch.int32, device=self.device)
         self._rows: dict[int, int] = {}
         self._free_rows = list(range(max_seqs - 1, -1, -1))
-        # host upper bound on any head's context length, per row (no sync)
-        self.ctx_bound = [0] * max_seqs
+        # host upper bound on any head's context length, per (row, layer) (no sync)
+        self.ctx_bound = CtxBound(max_seqs, num_layers)
 
     # -- capacity ---------------------------------------------------------------
 
@@ -141,7 +170,7 @@ class BlockTables:
     def set_context_len(self, seq_id: int, layer: int, head: int, value: int) -> None:
         row = self._rows[seq_id]
         self.ctx[row, layer, head] = value
-        self.ctx_bound[row] = max(self.ctx_bound[row], int(value))
+        self.ctx_bound.a[row, layer] = max(int(self.ctx_bound.a[row, layer]), int(value))
 
     def heads(self, seq_id: int) -> Iterator[tuple[int, int]]:
         for layer in range(self.num_layers):

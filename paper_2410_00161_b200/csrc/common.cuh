@@ -52,6 +52,24 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4 &v, float *f) {
   }
 }
 
+__device__ __forceinline__ void bf16x4_to_f32(const uint2 &v, float *f) {
+  f[0] = __uint_as_float(v.x << 16);
+  f[1] = __uint_as_float(v.x & 0xffff0000u);
+  f[2] = __uint_as_float(v.y << 16);
+  f[3] = __uint_as_float(v.y & 0xffff0000u);
+}
+
+// V consecutive bf16 values as one vector load (V = 8: 16 bytes, 4: 8 bytes)
+template <int V> struct BfVec;
+template <> struct BfVec<8> {
+  using T = uint4;
+  static __device__ __forceinline__ void to_f32(const T &v, float *f) { bf16x8_to_f32(v, f); }
+};
+template <> struct BfVec<4> {
+  using T = uint2;
+  static __device__ __forceinline__ void to_f32(const T &v, float *f) { bf16x4_to_f32(v, f); }
+};
+
 __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) {
   return __uint_as_float(((uint32_t)b) << 16);
 }

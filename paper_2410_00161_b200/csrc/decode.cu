@@ -80,7 +80,9 @@ __host__ __device__ inline SmemLayout smem_layout(int block_size, int chunk) {
 
 template <int D, int RMAX>
 __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P) {
-  constexpr int LPT = D / 8;         // lanes per token row (16 B per lane)
+  constexpr int kVec = D >= 8 ? 8 : D;  // bf16 per lane and vector load (16 B; 8 B at d = 4)
+  using VT = typename BfVec<kVec>::T;
+  constexpr int LPT = D / kVec;      // lanes per token row
   constexpr int TPP = 32 / LPT;      // tokens per warp pass
   extern __shared__ __align__(128) uint8_t smem[];
   const kvc_pool &p = P.p;
@@ -110,8 +112,10 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
   const int cp = c_old + (append ? 1 : 0);
   const bool multi = P.splits > 1;
 
-  // Uniform early exits (identical for every CTA of the cluster).
-  if (cp < 1 || (append && c_old >= nb * b) || cp > nb * b) {
+  // Uniform early exits (identical for every CTA of the cluster).  C beyond
+  // the caller's max_ctx bound (chunks x splits) would be silently truncated:
+  // reported as cache corruption instead.
+  if (cp < 1 || (append && c_old >= nb * b) || cp > nb * b || cp > P.chunk * P.splits) {
     if (split == 0 && threadIdx.x == 0) {
       if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
       else if (append && c_old >= nb * b) set_status(p.status, KVC_DEV_ALLOCATION_ORDER, (int32_t)hidx, c_old);
@@ -138,21 +142,21 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
   // Query fragment: dims [sub*8, sub*8+8) of every head in the group.
   const int sub = lane % LPT;
   const int grp = lane / LPT;
-  float qf[RMAX][8];
+  float qf[RMAX][kVec];
   bool bad_q = false;
 #pragma unroll
   for (int h = 0; h < RMAX; ++h) {
     if (h < P.r) {
-      const uint4 v = *reinterpret_cast<const uint4 *>(P.q + ((int64_t)bi * n_q + head * P.r + h) * D + sub * 8);
-      bf16x8_to_f32(v, qf[h]);
+      const VT v = *reinterpret_cast<const VT *>(P.q + ((int64_t)bi * n_q + head * P.r + h) * D + sub * kVec);
+      BfVec<kVec>::to_f32(v, qf[h]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < kVec; ++i) {
         bad_q |= !isfinite(qf[h][i]);
         qf[h][i] *= P.q_scale;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) qf[h][i] = 0.f;
+      for (int i = 0; i < kVec; ++i) qf[h][i] = 0.f;
     }
   }
   if (bad_q && split == 0) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
@@ -192,11 +196,11 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
       const int64_t slot = (int64_t)tab[blk] * b + off;
       const uint16_t *kn = P.k_new + ((int64_t)bi * heads + head) * D;
       const uint16_t *vn = P.v_new + ((int64_t)bi * heads + head) * D;
-      for (int i = lane; i < D / 8; i += 32) {
-        const uint4 kv = reinterpret_cast<const uint4 *>(kn)[i];
-        reinterpret_cast<uint4 *>(buf + off * D * 2)[i] = kv;
-        reinterpret_cast<uint4 *>(const_cast<uint16_t *>(kbase) + slot * D)[i] = kv;
-        reinterpret_cast<uint4 *>(const_cast<uint16_t *>(vbase) + slot * D)[i] = reinterpret_cast<const uint4 *>(vn)[i];
+      for (int i = lane; i < D / kVec; i += 32) {
+        const VT kv = reinterpret_cast<const VT *>(kn)[i];
+        reinterpret_cast<VT *>(buf + off * D * 2)[i] = kv;
+        reinterpret_cast<VT *>(const_cast<uint16_t *>(kbase) + slot * D)[i] = kv;
+        reinterpret_cast<VT *>(const_cast<uint16_t *>(vbase) + slot * D)[i] = reinterpret_cast<const VT *>(vn)[i];
       }
       __syncwarp();
     }
@@ -206,13 +210,13 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
 #pragma unroll
       for (int h = 0; h < RMAX; ++h) acc[h] = 0.f;
       if (t < valid) {
-        const uint4 kv = *reinterpret_cast<const uint4 *>(buf + t * D * 2 + sub * 16);
-        float kf[8];
-        bf16x8_to_f32(kv, kf);
+        const VT kv = *reinterpret_cast<const VT *>(buf + t * D * 2 + sub * kVec * 2);
+        float kf[kVec];
+        BfVec<kVec>::to_f32(kv, kf);
 #pragma unroll
         for (int h = 0; h < RMAX; ++h)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[h] = fmaf(qf[h][i], kf[i], acc[h]);
+          for (int i = 0; i < kVec; ++i) acc[h] = fmaf(qf[h][i], kf[i], acc[h]);
       }
 #pragma unroll
       for (int h = 0; h < RMAX; ++h) {
@@ -293,11 +297,11 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
   }
 
   // ---------------- pass B: P.V ----------------
-  float acc[RMAX][8];
+  float acc[RMAX][kVec];
 #pragma unroll
   for (int h = 0; h < RMAX; ++h)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[h][i] = 0.f;
+    for (int i = 0; i < kVec; ++i) acc[h][i] = 0.f;
   for (int it = 0; it < my_blocks; ++it, ++use) {
     const int stage = use % kStages;
     mbar_wait(&my_bars[stage], (use / kStages) & 1);
@@ -308,20 +312,20 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
     if (append && c_old >= tb0 && c_old < tb0 + b) {
       const int off = c_old - tb0;
       const uint16_t *vn = P.v_new + ((int64_t)bi * heads + head) * D;
-      for (int i = lane; i < D / 8; i += 32)
-        reinterpret_cast<uint4 *>(buf + off * D * 2)[i] = reinterpret_cast<const uint4 *>(vn)[i];
+      for (int i = lane; i < D / kVec; i += 32)
+        reinterpret_cast<VT *>(buf + off * D * 2)[i] = reinterpret_cast<const VT *>(vn)[i];
       __syncwarp();
     }
     for (int t = grp; t < valid; t += TPP) {
-      const uint4 vv = *reinterpret_cast<const uint4 *>(buf + t * D * 2 + sub * 16);
-      float vf[8];
-      bf16x8_to_f32(vv, vf);
+      const VT vv = *reinterpret_cast<const VT *>(buf + t * D * 2 + sub * kVec * 2);
+      float vf[kVec];
+      BfVec<kVec>::to_f32(vv, vf);
       const float *prow = scores + (tb0 - t0 + t) * RMAX;
 #pragma unroll
       for (int h = 0; h < RMAX; ++h) {
         const float pw = h < P.r ? prow[h] : 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[h][i] = fmaf(pw, vf[i], acc[h][i]);
+        for (int i = 0; i < kVec; ++i) acc[h][i] = fmaf(pw, vf[i], acc[h][i]);
       }
     }
     __syncwarp();
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
 #pragma unroll
   for (int h = 0; h < RMAX; ++h)
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kVec; ++i)
 #pragma unroll
       for (int o = LPT; o < 32; o <<= 1) acc[h][i] += __shfl_xor_sync(0xffffffffu, acc[h][i], o);
   __syncthreads();  // ring no longer in use by any warp
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_paged_decode(const DecodeParams P)
 #pragma unroll
     for (int h = 0; h < RMAX; ++h)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) opart[(warp * RMAX + h) * D + sub * 8 + i] = acc[h][i];
+      for (int i = 0; i < kVec; ++i) opart[(warp * RMAX + h) * D + sub * kVec + i] = acc[h][i];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < RMAX * D; e += kThreads) {
@@ -643,6 +647,7 @@ int kvc_paged_decode(const kvc_pool *pool, const kvc_decode_args *a, void *strea
   P.q_scale = 1.4426950408889634f / sqrtf((float)D);
   cudaStream_t s = (cudaStream_t)stream;
   switch (D) {
+    case 4: return dispatch_r<4>(P, a->batch, s);
     case 8: return dispatch_r<8>(P, a->batch, s);
     case 16: return dispatch_r<16>(P, a->batch, s);
     case 32: return dispatch_r<32>(P, a->batch, s);

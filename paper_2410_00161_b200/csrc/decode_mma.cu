@@ -251,11 +251,13 @@ __global__ void __launch_bounds__(kThreads) k_decode_stream(const __grid_constan
     }
   };
   if (P.early_pull) {
-    // First pull and its TMA loads before the dependency wait: the host
-    // allows this only when the kernel this one overlaps is the previous
-    // launch's kernel B for another layer, which writes none of what the
-    // pull reads (this launch's queue head, C, tables, rows); queries are
-    // read after the wait.
+    // First pull and its TMA loads before the dependency wait.  Only when
+    // the caller guarantees (kvc_decode_args.early_pull) that the kernel in
+    // front of this one is kernel B of another layer's launch over the same
+    // queue: that kernel writes none of what the pull reads (this launch's
+    // queue head - the heads alternate per launch -, this layer's C, tables,
+    // rows).  Never after the allocator, compaction or a scatter, which do
+    // write tables/nblocks/ctx.  Queries are read after the wait.
     if (lane == 0) wit[1].id = -1;
     fetch_item(P, wit[0], lane);
     if (lane == 0) try_issue();
@@ -583,10 +585,13 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   pdl_trigger();
   if (pair == 0 && slice == 0 && threadIdx.x == 0) *P.counter = 0;  // queue head for the next launch
   if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
-  if (cp < 1 || cp > cap) {  // no item ran for this head
+  if (cp < 1 || cp > cap || cp > P.max_ctx_pad) {  // no item ran (or not all of it) for this head
     if (slice == 0 && threadIdx.x == 0) {
       if (cp < 1) set_status(p.status, KVC_DEV_EMPTY_CONTEXT, (int32_t)hidx, 0);
-      else set_status(p.status, append ? KVC_DEV_ALLOCATION_ORDER : KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, c_old);
+      else if (cp > cap)
+        set_status(p.status, append ? KVC_DEV_ALLOCATION_ORDER : KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, c_old);
+      else  // C beyond the caller's max_ctx bound: the work items and score rows do not cover it
+        set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, cp);
     }
     return;
   }
@@ -730,7 +735,8 @@ __global__ void __launch_bounds__(256) k_decode_metric(const Params P) {
   const bool append = P.k_new != nullptr;
   const int cp = p.ctx[hidx];
   const int c_old = cp - (append ? 1 : 0);
-  if (cp < 1 || cp > p.nblocks[hidx] * kBlk) return;
+  // (kernel B rejected heads beyond max_ctx without bumping C)
+  if (cp < 1 || cp > p.nblocks[hidx] * kBlk || cp > P.max_ctx_pad || p.status[0] == KVC_DEV_CACHE_CORRUPTION) return;
   const int nck = (cp + P.item_tok - 1) / P.item_tok;
   const float *pml = P.part_ml + (int64_t)pair * P.n_ck * 2 * kHP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -922,6 +928,22 @@ int launch(Params &P, cudaStream_t s) {
 
 }  // namespace kvc_mma
 
+// Per-(device, stream) launch log: launches so far (queue-head parity) and the
+// layer of the last one.
+struct StreamKeyHash {
+  size_t operator()(const std::pair<int, cudaStream_t> &k) const {
+    return std::hash<void *>()(reinterpret_cast<void *>(k.second)) * 31u + (size_t)k.first;
+  }
+};
+static std::mutex &launch_mu() {
+  static std::mutex mu;
+  return mu;
+}
+static std::unordered_map<std::pair<int, cudaStream_t>, std::pair<long long, int>, StreamKeyHash> &launch_log() {
+  static std::unordered_map<std::pair<int, cudaStream_t>, std::pair<long long, int>, StreamKeyHash> m;
+  return m;
+}
+
 // Workspace bytes the fast path needs (scores + partials + queue head).
 static int64_t kvc_decode_mma_scratch(const kvc_pool *pool, int batch, int r, int max_ctx) {
   using namespace kvc_mma;
@@ -979,20 +1001,26 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   // from its head while the previous launch's kernel B still runs), then
   // the per-pair counters
   int *qbase = a->queue ? a->queue : reinterpret_cast<int *>(base);
+  // Queue-head parity alternates per launch on a (device, stream): a launch
+  // pulling early from its head must not share it with the previous launch,
+  // whose kernel B resets that head after its trigger.  The early pull itself
+  // is the caller's promise (a->early_pull: the work right before this call on
+  // the stream is kernel B of another layer over the same queue - e.g. layer
+  // m > 0 of a DecodeStepGraph step); the host adds what it can check.  The
+  // launch count is committed only after a successful launch.
+  int dev_id = 0;
+  cudaGetDevice(&dev_id);
+  const std::pair<int, cudaStream_t> skey{dev_id, s};
   int parity = 0;
   bool early = false;
   {
-    static std::mutex mu;
-    static std::unordered_map<cudaStream_t, std::pair<long long, int>> last;  // launches, last layer
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = last.find(s);
+    std::lock_guard<std::mutex> lk(launch_mu());
+    auto &last = launch_log();
+    auto it = last.find(skey);
     const long long n_prev = it == last.end() ? 0 : it->second.first;
     const int layer_prev = it == last.end() ? -1 : it->second.second;
     parity = (int)(n_prev & 1);
-    // the kernel A of this launch overlaps the previous launch's kernel B on
-    // this stream: safe to pull early unless that one bumped this layer's C
-    early = a->queue && layer_prev >= 0 && layer_prev != a->layer && !getenv("KVC_NO_EARLY_PULL");
-    last[s] = {n_prev + 1, a->layer};
+    early = a->early_pull && a->queue && layer_prev >= 0 && layer_prev != a->layer && !getenv("KVC_NO_EARLY_PULL");
   }
   P.counter = qbase + parity;
   P.pair_done = qbase + 2;
@@ -1014,9 +1042,17 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
       P.trace = tbuf;
     }
   }
+  int rc;
   switch (D) {
-    case 64: return launch<64>(P, s);
-    case 128: return launch<128>(P, s);
-    default: return launch<256>(P, s);
+    case 64: rc = launch<64>(P, s); break;
+    case 128: rc = launch<128>(P, s); break;
+    default: rc = launch<256>(P, s); break;
   }
+  if (rc == KVC_OK) {
+    std::lock_guard<std::mutex> lk(launch_mu());
+    auto &e = launch_log()[skey];
+    e.first += 1;
+    e.second = a->layer;
+  }
+  return rc;
 }

@@ -134,6 +134,9 @@ class DecodeStepGraph:
             a.splits = 0
             a.queue = self.queue.data_ptr()
             a.metric_stream = self.side.cuda_stream if self.side is not None else None
+            # layer m > 0 follows layer m-1's kernel B directly on the stream;
+            # layer 0 follows the allocator, which writes tables / nblocks
+            a.early_pull = int(m > 0)
             args.append(a)
         self._keep = (pools, args)
         self.graphs = {}
@@ -251,8 +254,7 @@ class DecodeStepGraph:
         if io not in self.graphs:
             self._capture(io)
         self.graphs[io].replay()
-        for r in self.rows:
-            self.tables.ctx_bound[r] += 1
+        self.tables.ctx_bound.bump_rows(self.rows)
         self.replays += 1
         return self.out if h is None else h["out"]
 
@@ -263,5 +265,5 @@ class DecodeStepGraph:
         for m in range(self.tables.num_layers):
             paged_decode(self.q[m], self.cache, self.tables, None, m, self.cfg, store=self.store,
                          metric_mode=self.metric_mode, k_new=self.k_new[m], v_new=self.v_new[m], fresh=self.fresh,
-                         out=self.out[m], rows_tensor=self.rows_t, host_rows=self.rows)
+                         out=self.out[m], rows_tensor=self.rows_t, host_rows=self.rows, early_pull=m > 0)
         self.store.clear_fresh(self.tables, self.seq_ids)

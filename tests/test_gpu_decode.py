@@ -41,7 +41,7 @@ def test_library_loads_with_every_symbol():
     from paper_2410_00161_b200 import _lib
 
     lib = _lib.load()
-    assert lib.kvc_abi_version() == 1
+    assert lib.kvc_abi_version() == 2
     for name in _lib.EXPORTED:
         assert hasattr(lib, name)
 
@@ -82,8 +82,6 @@ def test_allocator_matches_reference_trace(i):
 def test_paged_attention_golden(i):
     """paged_attention + accumulate_decode on the reference's golden inputs."""
     case = load("decode_cases.json")[i]
-    if case["head_dim"] < 8:
-        pytest.skip("kernels are compiled for head_dim >= 8")
     st = state_from_snapshot(case["before"], case["num_blocks"], case["block_size"],
                              case["head_dim"], case["layers"], case["heads"])
     st.keys = bf16_round(st.keys)
@@ -270,3 +268,51 @@ def test_decode_bench_scale_path():
     dst = rig.to_oracle()
     assert_same_ints(dst, st)
     assert np.allclose(dst.metric, st.metric, rtol=MET_RTOL, atol=1e-6)
+
+
+@pytest.mark.parametrize("d", [128, 8])
+def test_context_beyond_host_bound_raises(d):
+    """A caller that writes tables.ctx directly (the reference tests' idiom)
+    past the host bound the launch is sized from: the kernels report
+    CacheCorruptionError instead of silently attending a truncated context
+    (fast path d = 128: items x score rows; generic path d = 8: chunks)."""
+    b, heads, r = 16, 1, 4
+    rig = DevRig(128, b, d, 1, heads)
+    cfg = K.AttentionConfig(heads * r, heads, d, 1)
+    rig.manager.allocate_prefill(0, 64 * b)            # 64 blocks = 1024 slots per head
+    rig.tables.set_context_len(0, 0, 0, 100)           # host bound 100
+    row = rig.tables.row(0)
+    rig.tables.ctx[row, 0, 0] = 900                    # raw write, bound not raised
+    q = torch.zeros((1, heads * r, d), dtype=torch.bfloat16, device="cuda")
+    K.paged_decode(q, rig.cache, rig.tables, [0], 0, cfg)
+    from paper_2410_00161_b200 import _lib
+    with pytest.raises(E.CacheCorruptionError):
+        _lib.DeviceContext.get(rig.cache.device).raise_status()
+    # within the bound it runs
+    rig.tables.set_context_len(0, 0, 0, 900)
+    K.paged_decode(q, rig.cache, rig.tables, [0], 0, cfg)
+    _lib.DeviceContext.get(rig.cache.device).raise_status()
+
+
+def test_decode_step_raises_bound_once_per_step():
+    """paged_decode over every layer of a step raises the row's host context
+    bound by one, not by the number of layers (scratch and tables are sized
+    from it)."""
+    rng = np.random.default_rng(11)
+    b, d, heads, r, layers = 16, 64, 2, 2, 4
+    st = random_state(rng, 1024, b, d, layers, heads, [0], 100, min_len=50)
+    rig = DevRig(1024, b, d, layers, heads)
+    rig.load(st)
+    cfg = K.AttentionConfig(heads * r, heads, d, layers)
+    row = rig.tables.row(0)
+    before = rig.tables.ctx_bound[row]
+    dev = rig.cache.device
+    for _ in range(3):
+        rig.manager.allocate_decode_step([0])
+        for m in range(layers):
+            q = torch.zeros((1, heads * r, d), dtype=torch.bfloat16, device=dev)
+            kv = torch.zeros((1, heads, d), dtype=torch.bfloat16, device=dev)
+            K.paged_decode(q, rig.cache, rig.tables, [0], m, cfg, store=rig.store, metric_mode=2, k_new=kv,
+                           v_new=kv)
+    assert rig.tables.ctx_bound[row] == before + 3
+    assert int(rig.tables.ctx[row].max()) <= before + 3

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.kvc_abi_version() == 1
+    assert lib.kvc_abi_version() == 2
     assert lib.kvc_status_name(1).decode() == "PreemptionNeeded"
 
 
@@ -42,7 +42,8 @@ def test_ctypes_layout_matches_c():
     from paper_2410_00161_b200 import _lib
 
     structs = {"kvc_pool": _lib.KvcPool, "kvc_decode_args": _lib.DecodeArgs,
-               "kvc_window_args": _lib.WindowArgs, "kvc_evict_args": _lib.EvictArgs}
+               "kvc_window_args": _lib.WindowArgs, "kvc_evict_args": _lib.EvictArgs,
+               "kvc_full_args": _lib.FullArgs}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
