@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-fragmented", action="store_true", help="skip the random-placement decode measurement")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the decode step layer by layer instead of replaying its CUDA graph")
+    ap.add_argument("--save-ctx", action="store_true",
+                    help="write the decode's per-head starting contexts to profiles/ctx_<preset>_b<B>.json "
+                         "(the reference arm decodes the same ragged lengths)")
     ap.add_argument("--preset", default="l8b", choices=sorted(PRESETS),
                     help="BASELINE.json config the shape flags default to (explicit flags override)")
     args = ap.parse_args()
@@ -220,16 +223,21 @@ def eviction_rounds(S, args):
         del k, v
         S["_lib"].DeviceContext.get(dev).raise_status()
         E = K.budget_to_blocks(S["keep_tokens"], l, H, b, tables.sequence_block_count(s))
-        e0, e1 = ev(), ev()
+        e0, e1, e2 = ev(), ev(), ev()
         torch.cuda.synchronize()
         plan = K.compress(cache, tables, manager, store, {s: E}, sync=False, events=(e0, e1))
+        # the round's only cross-GPU traffic: all-gather of every rank's
+        # (freed, evicted, moves, free) counters, stream-ordered under NCCL
+        out["rank_counts"] = K.gather_round_counts(plan.totals)
+        e2.record()
         torch.cuda.synchronize()
         S["_lib"].DeviceContext.get(dev).raise_status()
         tot = plan.totals.tolist()
         K.compression.refresh_ctx_bounds(tables, [s])
         out["k2_ms"].append(k2_t)
         out["scatter_ms"].append(sc_t)
-        out["k34_ms"].append(e0.elapsed_time(e1))
+        out["k34_ms"].append(e0.elapsed_time(e2))
+        out.setdefault("k34_kernels_ms", []).append(e0.elapsed_time(e1))
         out["freed"].append(tot[0])
         out["evicted"].append(tot[1])
         out["moves"].append(tot[2])
@@ -464,13 +472,15 @@ def decode_compression_rounds(S, args, rounds=2, gap_steps=8):
             _clear_fresh_rows(S, rows_t)
         nb = tables.nblocks[rows_t.long()].reshape(B, -1).sum(dim=1).tolist()
         budgets = {s: K.budget_to_blocks(S["keep_tokens"], l, H, b, int(nb[i])) for i, s in enumerate(seqs)}
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         torch.cuda.synchronize()
         plan = K.compress(cache, tables, manager, store, budgets, sync=False, events=(e0, e1))
+        K.gather_round_counts(plan.totals)
+        e2.record()
         torch.cuda.synchronize()
         S["_lib"].DeviceContext.get(dev).raise_status()
         K.compression.refresh_ctx_bounds(tables, seqs)
-        out["ms"].append(e0.elapsed_time(e1))
+        out["ms"].append(e0.elapsed_time(e2))
         out["freed"].append(int(plan.totals.tolist()[0]))
     return out
 
@@ -561,77 +571,209 @@ def cpu_window_sample(L, H, r, d, seed=0):
 # ---------------------------------------------------------------------------
 
 
-def config_dict(args, world):
+def config_dict(args, world, shared=False):
     return {"workload": PRESETS[args.preset]["workload"], "preset": args.preset,
             "batch_per_gpu": args.batch, "global_batch": args.batch * world, "context": args.context,
             "layers": args.layers, "kv_heads": args.kv_heads, "query_heads": args.kv_heads * args.group,
             "head_dim": args.head_dim, "block_size": 16, "compression": f"{args.rate:g}x",
-            "metric": "window w=8 p=7 L2 at prefill, L2 decode accumulation", "parallelism": f"seq-shard x{world}",
+            "metric": "window w=8 p=7 L2 at prefill, L2 decode accumulation",
+            "parallelism": f"seq-shard x{world}" + (" (ranks sharing one GPU: code-path check, not a measurement)"
+                                                      if shared else ""),
             "l2": "KV working set (>34 GB) >> 126 MB L2; no flush needed"}
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the oracle port (the reference is CPU Python) on all
-    host cores, bounded per-step samples of the same workload."""
-    if rank != 0:
-        return
+# ---------------------------------------------------------------------------
+# --impl reference: the reference's CPU path (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+
+
+def ctx_fixture_path(args):
+    return os.path.join(ROOT, "profiles", f"ctx_{args.preset}_b{args.batch}.json")
+
+
+def load_ctx_fixture(args):
+    """Per-(sequence, layer, head) contexts the GPU arm decodes from (its
+    ctx_before, saved by `bench.py --save-ctx`), or None."""
+    try:
+        with open(ctx_fixture_path(args)) as fh:
+            d = json.load(fh)
+        a = np.asarray(d["ctx_before"], dtype=np.int64)
+        if list(d["shape"]) == [args.batch, args.layers, args.kv_heads] and d["context"] == args.context \
+                and d["rate"] == args.rate:
+            return a.reshape(args.batch, args.layers, args.kv_heads)
+    except Exception:
+        pass
+    return None
+
+
+_REF = {}
+
+
+def _ref_worker_init(H, r, d, max_ctx, seed):
+    """A worker's oracle pool: random f64 K/V for 2 units of H heads at the
+    largest context (each unit is placed at random blocks of it)."""
+    from oracle import kvc_oracle as O
+
+    b = 16
+    nb = -(-(max_ctx + 1) // b)
+    st = O.OracleState(2 * H * nb + 8, b, d, 1, H)
+    rng = np.random.default_rng(seed + os.getpid())
+    st.keys[:] = rng.standard_normal(st.keys.shape)
+    st.values[:] = rng.standard_normal(st.values.shape)
+    st.tables[0] = [[[] for _ in range(H)]]
+    st.ctx[0] = np.zeros((1, H), dtype=np.int64)
+    _REF.update(O=O, st=st, rng=rng, b=b, r=r)
+
+
+def _ref_units(units):
+    """The reference decode of (seq, layer) units, each = per-head contexts:
+    append the step's K/V to every head, attend in table order, fold the L2
+    mass into the metrics (engine.py:426-444: append_kv, paged_attention,
+    accumulate_decode), then undo the append so every step has the same size."""
+    O, st, rng, b = _REF["O"], _REF["st"], _REF["rng"], _REF["b"]
+    H, d = st.num_kv_heads, st.head_dim
+    r = _REF["r"]
+    perm = rng.permutation(st.num_blocks)
+    for ctx_heads in units:
+        pos = 0
+        for h, c in enumerate(ctx_heads):
+            nb = -(-(int(c) + 1) // b)
+            st.tables[0][0][h] = perm[pos: pos + nb].tolist()
+            pos += nb
+            st.ctx[0][0, h] = int(c)
+        q = rng.standard_normal((H * r, d))
+        kn = rng.standard_normal((H, d))
+        O.decode_step_layer(st, 0, 0, q, kn, kn, "L2")
+        st.ctx[0][0] -= 1
+        perm = np.roll(perm, pos)
+    return len(units)
+
+
+def run_reference(args, world):
+    """--impl reference: full decode steps of the reference algorithm (the
+    oracle port of attention.py:92-127 + metrics.py:189-211, float64 NumPy),
+    B sequences x l layers of (sequence, layer) units per step, on every
+    host core (one process per core, one BLAS thread each), over the same
+    ragged per-head contexts the GPU arm decodes (profiles/ctx_*.json, saved
+    from the GPU arm).  At N > 1 a step is one rank's share (B sequences)
+    and the job time is that x N (a bounded sample)."""
     import multiprocessing as mp
+    import platform
 
     cores = os.cpu_count() or 1
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"  # one BLAS thread per worker process: no oversubscription
-    L, H, r, d, l = args.context, args.kv_heads, args.group, args.head_dim, args.layers
-    ctx_heads = [int(L / args.rate)] * H  # uniform control lengths
-    per = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
-    with mp.get_context("spawn").Pool(cores) as pool:
-        t_steps = []
+    L, H, r, d, l, B = args.context, args.kv_heads, args.group, args.head_dim, args.layers, args.batch
+    ctx = load_ctx_fixture(args)
+    ragged = ctx is not None
+    if ctx is None:
+        ctx = np.full((B, l, H), int(L / args.rate), dtype=np.int64)
+    units = [ctx[s, m].tolist() for s in range(B) for m in range(l)]
+    n_chunks = min(len(units), cores * 4)
+    chunks = [units[i::n_chunks] for i in range(n_chunks)]
+    cpu_model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), cpu_model)
+    except Exception:
+        pass
+    t_steps = []
+    with mp.get_context("spawn").Pool(cores, initializer=_ref_worker_init,
+                                      initargs=(H, r, d, int(ctx.max()) + 1, 17)) as pool:
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            res = pool.starmap(cpu_decode_sample, [(ctx_heads, d, r, H, per / 2, i * cores + c) for c in range(cores)])
-            t_steps.append(float(np.mean(res)))
-    t_sl = float(np.mean(t_steps[args.warmup:]))
-    # one decode step = B sequences x l layers of (seq, layer) work, spread over `cores`
-    step_s = args.batch * l * t_sl / cores
-    value = args.batch / step_s
+            done = sum(pool.map(_ref_units, chunks, chunksize=1))
+            t_steps.append(time.perf_counter() - t0)
+            assert done == len(units)
+    step_s = float(np.mean(t_steps[args.warmup:])) * world
+    value = B * world / step_s
+    sample = (f"full decode steps: {B} sequences x {l} layers = {len(units)} (seq, layer) units of oracle "
+              f"decode_step_layer (append + paged attention + L2 accumulate, f64) per step, {H} heads, d={d}, "
+              + (f"ragged per-head C from the GPU arm's compressed state (mean {ctx.mean():.0f}, "
+                 f"{os.path.basename(ctx_fixture_path(args))})" if ragged else f"uniform C={int(L / args.rate)}")
+              + f"; {cores} worker processes x 1 BLAS thread on '{cpu_model}'"
+              + (f"; N={world}: one rank's share per step, job time x{world}" if world > 1 else ""))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config_dict(args, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"oracle decode_step_layer (append+attend+L2 accumulate) of one (seq, layer) "
-                                       f"with {H} heads x C={ctx_heads[0]} at d={d}, per core, ~{per:.1f}s per step; "
-                                       f"extrapolated x{args.batch}x{l}/{cores} cores"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model, "step_s": t_steps[args.warmup:]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) on
+    this node and exit with their status."""
+    import socket
+
+    import torch
+
+    shared = os.environ.get("KVC_BENCH_SHARE_GPU") == "1"
+    have = torch.cuda.device_count()
+    if have < args.gpus and not shared:
+        sys.exit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world_env = os.environ.get("WORLD_SIZE")
+    world = int(world_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        if rank == 0:  # rank 0 alone times the CPU path; the other ranks exit 0
+            run_reference(args, world if world_env else args.gpus)
         return
+    if world_env is None and args.gpus > 1:
+        relaunch(args)
+        return
+    if world != args.gpus:
+        sys.exit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     import torch
 
+    # ranks sharing one GPU (KVC_BENCH_SHARE_GPU=1, gloo): exercises the
+    # multi-rank code path on a 1-GPU box; its numbers are not measurements
+    shared = os.environ.get("KVC_BENCH_SHARE_GPU") == "1"
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
 
-        torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl")
+        if not shared and torch.cuda.device_count() < world:
+            sys.exit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} CUDA device(s) visible")
+        # NCCL's init log (rank / device / transport lines) goes to stderr so the
+        # JSON line stays the last line of stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        torch.cuda.set_device(0 if shared else local)
+        dist_mod.init_process_group("gloo" if shared else "nccl", device_id=None if shared else
+                                    torch.device("cuda", local))
         dist = dist_mod
     dev = torch.device("cuda", torch.cuda.current_device())
     S = build(args, dev, rank)
     S["dist"] = dist
     ev = eviction_rounds(S, args)
     populate(S, args)
-    if dist is not None:
-        from paper_2410_00161_b200.sharding import gather_round_counts
-
-        gather_round_counts(S["manager"], [sum(ev["freed"]), sum(ev["evicted"]), sum(ev["moves"])])
     dec = decode_bench(S, args)
+    if args.save_ctx and rank == 0:
+        with open(ctx_fixture_path(args), "w") as fh:
+            json.dump({"shape": [args.batch, args.layers, args.kv_heads], "context": args.context, "rate": args.rate,
+                       "what": "per-(sequence, layer, head) context C the GPU arm's timed decode starts from "
+                               "(3 real prefill->K2->K3->K4 rounds, copied round-robin to the batch)",
+                       "ctx_before": dec["ctx_before"].tolist()}, fh)
     e2e = None if args.no_e2e else decode_bench(S, args, e2e=True)
     dcr = decode_compression_rounds(S, args)
     # last: the same decode with every block of the batch at a random place in
@@ -642,69 +784,86 @@ def main():
         fsteps = max(3, min(args.steps, 5))
         fargs = argparse.Namespace(**{**vars(args), "steps": fsteps})
         frag = decode_bench(S, fargs)
-        frag = {"value": args.batch * world * fsteps / (frag["ms"] * 1e-3), "unit": UNIT,
-                "ms_per_step": frag["ms"] / fsteps, "steps": fsteps,
-                "what": "same decode step with the batch's blocks randomly permuted over the pool "
-                        "(fragmented placement; the default line is the allocator's contiguous placement)"}
-    ms = dec["ms"]
-    ms_e2e = e2e["ms"] if e2e else None
-    if dist is not None:
-        t = torch.tensor([ms, ms_e2e or 0.0], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_e2e = float(t[0]), (float(t[1]) if e2e else None)
+        frag["steps"] = fsteps
+    timed = slice(1, None) if len(ev["k2_ms"]) > 1 else slice(None)
+    mine = {"ms": dec["ms"], "ms_e2e": e2e["ms"] if e2e else None, "frag_ms": frag["ms"] if frag else None,
+            "k2": float(np.mean(ev["k2_ms"][timed])), "k34": float(np.mean(ev["k34_ms"][timed])),
+            "k34_kernels": float(np.mean(ev["k34_kernels_ms"][timed])),
+            "scatter": float(np.mean(ev["scatter_ms"][timed])),
+            "fused": float(np.mean(ev["fused_ms"][timed])) if ev["fused_ms"] else None,
+            "dcr": dcr["ms"][-1], "clocks": dec["clocks"]}
+    if dist is not None:  # every rank's numbers to every rank; times are the max over ranks
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+    else:
+        allr = [mine]
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
         return
+    tmax = lambda k: max(x[k] for x in allr) if allr[0][k] is not None else None
+    rank_counts = ev["rank_counts"].cpu().tolist() if torch.is_tensor(ev["rank_counts"]) else ev["rank_counts"]
     B, steps = args.batch, args.steps
+    ms, ms_e2e = tmax("ms"), tmax("ms_e2e")
     value = B * world * steps / (ms * 1e-3)
     peak, peak_kind = peaks()
     step_ms = ms / steps
-    # the first round pays one-time costs (attribute setup, tensor-map encodes): report the others
-    timed = slice(1, None) if len(ev["k2_ms"]) > 1 else slice(None)
-    k2 = float(np.mean(ev["k2_ms"][timed])) if ev["k2_ms"] else None
-    k34 = float(np.mean(ev["k34_ms"][timed])) if ev["k34_ms"] else None
+    k2, k34, k34k, scat, fused = tmax("k2"), tmax("k34"), tmax("k34_kernels"), tmax("scatter"), tmax("fused")
     evict = {
         "per_sequence_ms": {"k2_window_metric": k2, "k3k4_schedule_compact": k34,
-                            "total": (k2 or 0) + (k34 or 0), "kv_scatter_not_counted": float(np.mean(ev["scatter_ms"][timed]))},
+                            "k3k4_kernels_only": k34k, "total": k2 + k34, "kv_scatter_not_counted": scat,
+                            "what": "k3k4 includes the per-round NCCL all-gather of (freed, evicted, moves, free) "
+                                    "counters (world > 1); max over ranks"},
         "freed_blocks": ev["freed"], "moves": ev["moves"], "evicted_kvs": ev["evicted"],
+        "rank_counts_last_round": rank_counts,
         "rounds_ms": {"k2": ev["k2_ms"], "k3k4": ev["k34_ms"], "first_round_is_warmup": len(ev["k2_ms"]) > 1},
         "prefill_side_per_sequence_ms": {
             "what": "prompt K/V into the cache + window metric + compress to the budget, per new sequence",
-            "unfused_scatter_k2_k3k4": float(np.mean(ev["scatter_ms"][timed])) + (k2 or 0) + (k34 or 0),
-            "fused_prefill_compress": float(np.mean(ev["fused_ms"][timed])) if ev["fused_ms"] else None,
+            "unfused_scatter_k2_k3k4": scat + k2 + k34, "fused_prefill_compress": fused,
             "fused_rounds_ms": ev["fused_ms"]},
         "ratio_to_decode_step": {
-            "raw_with_k2": ((k2 or 0) + (k34 or 0)) / step_ms, "raw_without_k2": (k34 or 0) / step_ms,
-            "amortised_500_tokens_with_k2": ((k2 or 0) + (k34 or 0)) * B / 500 / step_ms},
+            "raw_with_k2": (k2 + k34) / step_ms, "raw_without_k2": k34 / step_ms,
+            "amortised_500_tokens_with_k2": (k2 + k34) * B / 500 / step_ms},
         "decode_round": {
             "what": f"every-step policy: one compress() over all {B} running sequences "
                     f"(K3+K4, decode-accumulated L2 metric), {8} decode steps after the previous round",
-            "ms": dcr["ms"], "freed_blocks": dcr["freed"],
-            "ratio_to_decode_step": dcr["ms"][-1] / step_ms},
+            "ms": tmax("dcr"), "freed_blocks": dcr["freed"], "ratio_to_decode_step": tmax("dcr") / step_ms},
     }
-    if ev["fused_ms"]:
+    if fused is not None:
         # on-prefill policy: the metric -> schedule -> compact step fused into the
         # prompt write, minus the plain prompt write it replaces (can be < 0)
-        fused = float(np.mean(ev["fused_ms"][timed]))
-        scat = float(np.mean(ev["scatter_ms"][timed]))
         evict["fused_marginal_over_prompt_write"] = {
             "ms_per_sequence": fused - scat, "ratio_to_decode_step": (fused - scat) / step_ms,
             "what": "prefill_compress_sequence minus write_prefill_kv_layers for the same prompt"}
+    frag_line = None
+    if frag is not None:
+        fsteps = frag["steps"]
+        frag_line = {"value": B * world * fsteps / (tmax("frag_ms") * 1e-3), "unit": UNIT,
+                     "ms_per_step": tmax("frag_ms") / fsteps, "steps": fsteps,
+                     "what": "same decode step with the batch's blocks randomly permuted over the pool "
+                             "(fragmented placement; the default line is the allocator's contiguous placement)"}
+    # K1 bytes per launch are this rank's; with equal shards every rank moves the same
+    k1_gbs = dec["bytes_per_step"] / (step_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (unit-normal Q/K/V, random-init shapes; no checkpoints)", "config": config_dict(args, world),
-        "hbm_gbs_decode_step": dec["bytes_per_step"] / (step_ms * 1e-3) / 1e9,
+        "data": "synthetic (unit-normal Q/K/V, random-init shapes; no checkpoints)",
+        "config": config_dict(args, world, shared),
+        "per_rank_ms_per_step": [x["ms"] / steps for x in allr],
+        "hbm_gbs_decode_step": k1_gbs,
         "roofline": {"bound": "hbm",
                      "kernel": "K1 per layer: k_decode_stream + k_decode_finish (+ k_decode_metric, graph side branch)",
-                     "achieved": dec["k1_gbs"], "peak": peak, "unit": "GB/s", "frac": dec["k1_gbs"] / peak,
+                     "achieved": dec["k1_gbs"] if world == 1 else k1_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": (dec["k1_gbs"] if world == 1 else k1_gbs) / peak,
                      "peak_source": peak_kind, "traffic": k1_traffic(),
+                     "traffic_source": "profiles/r1_ncu.json: dram bytes of one K1 layer launch from a committed "
+                                       "ncu --set full capture (not measured in this run)",
                      "bytes_per_launch": dec["k1_bytes_mean"], "launch_ms": dec["k1_ms_mean"],
-                     "timing": dec["k1_timing"]},
+                     "timing": dec["k1_timing"] + ("; per GPU, slowest rank" if world > 1 else "")},
         "eviction_step": evict,
-        "fragmented_placement": frag,
+        "fragmented_placement": frag_line,
         "clocks": dec["clocks"],
+        "clocks_per_rank": [x["clocks"] for x in allr] if world > 1 else None,
         "gpu_launches": dec["launches_per_step"] * steps,
     }
     if e2e:

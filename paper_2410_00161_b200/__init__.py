@@ -29,6 +29,7 @@ from .metrics import MetricConfig, MetricsStore, accumulate_decode
 from .engine import POLICY_PRESETS, CompressionPolicy, Engine, StepRecord, select_compression_batch
 from .graph import DecodeStepGraph
 from .prefill import full_metrics, prefill_compress_sequence, prefill_sequence, window_metrics
+from .sharding import ShardedEngine, gather_counts, gather_round_counts, owner_of, shard_sequences
 
 __version__ = "0.1.0"
 
@@ -64,4 +65,9 @@ __all__ = [
     "full_metrics",
     "schedule_evictions",
     "window_metrics",
+    "ShardedEngine",
+    "gather_counts",
+    "gather_round_counts",
+    "owner_of",
+    "shard_sequences",
 ]

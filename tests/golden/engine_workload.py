@@ -46,4 +46,31 @@ CASES = [
      [(120, 10), (220, 14), (64, 20), (180, 9), (99, 16)]),
     ("no-compression-preemption", dict(policy="none", num_blocks=70, rate=1.0, budget_floor=128),
      [(64, 20), (64, 10), (48, 6)]),
+    # f4 policy coverage (engine.py:132-156, 282-289, 388-410):
+    # every-step rounds truncated by kv_limit (staleness order, stop at the
+    # first sequence that would exceed the limit)
+    ("kv-limit", dict(policy=dict(on_prefill=True, on_preempt=True, every_c=1, kv_limit=2000), num_blocks=400,
+                      rate=8.0, budget_floor=8),
+     [(120, 10), (220, 14), (64, 20), (180, 9), (99, 16)]),
+    # rounds triggered only by the uncompressed-token threshold
+    ("token-threshold", dict(policy=dict(on_prefill=False, on_preempt=False, token_threshold=30), num_blocks=400,
+                             rate=8.0, budget_floor=8),
+     [(120, 10), (220, 14), (64, 20), (180, 9), (99, 16)]),
+    # decode allocation runs dry: compress first, then preempt when that is
+    # not enough (same step)
+    ("decode-compress-then-preempt", dict(policy="prefill-preempt", num_blocks=52, rate=2.0, budget_floor=16),
+     [(40, 25), (45, 20), (50, 30), (35, 25)]),
 ]
+
+# multi-GPU: request i of a case runs on rank i % SHARD_WORLD (sharding.owner_of)
+SHARD_WORLD = 2
+
+
+def make_policy(mod, spec):
+    """Preset name or CompressionPolicy kwargs -> the module's policy object."""
+    return mod.POLICY_PRESETS[spec] if isinstance(spec, str) else mod.CompressionPolicy(**spec)
+
+
+def shard(reqs, rank, world=SHARD_WORLD):
+    """(global index, request) pairs rank `rank` owns."""
+    return [(i, r) for i, r in enumerate(reqs) if i % world == rank]
