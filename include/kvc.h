@@ -35,6 +35,9 @@
  *   kvc_compress            compress (both of the above)      compression.py:312-355
  *   kvc_prefill_compress    prefill scatter + compress fused  engine.py:340-358 + compression.py:312-355
  *   kvc_clear_fresh         MetricsStore.clear_fresh          metrics.py:185-186
+ *   kvc_gqa_attention       gqa_attention (dense causal GQA)  attention.py:62-89
+ *   kvc_attn_metrics        window_metrics / full_metrics on an attention tensor
+ *                                                             metrics.py:50-109
  */
 #ifndef KVC_H_
 #define KVC_H_
@@ -258,6 +261,41 @@ typedef struct kvc_full_args {
  * (attention.py:62-89) for one layer, on tcgen05: row statistics, then
  * column sums over rows i >= j + v.  Install with kvc_write_prompt_pass. */
 int kvc_full_metric(const kvc_pool *pool, const kvc_full_args *args, void *stream);
+
+/* ---- reference-signature metrics on an explicit attention tensor --------- */
+
+typedef struct kvc_dense_args {
+  int32_t num_query_heads;
+  int32_t L;
+  const float *q;           /* f32 [n_q][L][head_dim] */
+  const float *k;           /* f32 [heads][L][head_dim] */
+  const float *v;           /* f32 [heads][L][head_dim] or NULL (no output) */
+  float *out;               /* f32 [n_q][L][head_dim] or NULL */
+  float *attn;              /* f32 [n_q][L][L]: causal row softmax, 0 above the diagonal */
+} kvc_dense_args;
+
+/* gqa_attention (attention.py:62-89): query head h reads KV head h / r;
+ * fp32, max-subtracted softmax.  Non-finite scores -> KVC_DEV_NUMERIC.
+ * Materialises the (n_q, L, L) attention like the reference (L <= ~56k). */
+int kvc_gqa_attention(const kvc_pool *pool, const kvc_dense_args *args, void *stream);
+
+typedef struct kvc_attn_metric_args {
+  int32_t num_query_heads;
+  int32_t L;
+  const float *attn;        /* f32 [n_q][L][L] */
+  int32_t mode;             /* 0 window_metrics, 1 full_metrics */
+  int32_t window;           /* window mode: last `window` query rows */
+  int32_t pool;             /* window mode: odd max-pool width (scratch: heads*L f32 when > 1) */
+  int32_t excluded;         /* full mode: key j aggregates rows i >= j + excluded */
+  int32_t aggregation;      /* 1 L1, 2 L2 */
+  float *metrics_out;       /* f32 [heads][L] */
+} kvc_attn_metric_args;
+
+/* window_metrics (metrics.py:68-89) / full_metrics (metrics.py:92-109) of an
+ * attention tensor: group sums over each KV head's r query heads, then the
+ * centred max-pool (window mode).  The protected mask is the caller's
+ * (positions >= L - window unless protect_window is off). */
+int kvc_attn_metrics(const kvc_pool *pool, const kvc_attn_metric_args *args, void *stream);
 
 /* ---- K3 + K4: eviction schedule and compaction --------------------------- */
 

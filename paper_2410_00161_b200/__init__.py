@@ -7,7 +7,7 @@ libkvc.so (hand-written CUDA, C ABI in include/kvc.h); there is no CPU
 fallback.
 """
 
-from .attention import AttentionConfig, paged_attention, paged_decode
+from .attention import AttentionConfig, gqa_attention, paged_attention, paged_decode
 from .block_manager import BlockManager, blocks_needed_prefill
 from .budget import budget_to_blocks, per_sequence_budget
 from .cache import (
@@ -25,10 +25,10 @@ from .compression import (
     execute_cache_moves,
     schedule_evictions,
 )
-from .metrics import MetricConfig, MetricsStore, accumulate_decode
+from .metrics import MetricConfig, MetricsStore, accumulate_decode, full_metrics, prompt_metrics, window_metrics
 from .engine import POLICY_PRESETS, CompressionPolicy, Engine, StepRecord, select_compression_batch
 from .graph import DecodeStepGraph
-from .prefill import full_metrics, prefill_compress_sequence, prefill_sequence, window_metrics
+from .prefill import full_metrics_qk, prefill_compress_sequence, prefill_sequence, window_metrics_qk
 from .sharding import ShardedEngine, gather_counts, gather_round_counts, owner_of, shard_sequences
 
 __version__ = "0.1.0"
@@ -65,6 +65,10 @@ __all__ = [
     "full_metrics",
     "schedule_evictions",
     "window_metrics",
+    "window_metrics_qk",
+    "full_metrics_qk",
+    "prompt_metrics",
+    "gqa_attention",
     "ShardedEngine",
     "gather_counts",
     "gather_round_counts",

@@ -74,6 +74,19 @@ class FullArgs(ctypes.Structure):
     ]
 
 
+class DenseArgs(ctypes.Structure):
+    _fields_ = [
+        ("num_query_heads", _i32), ("L", _i32), ("q", _p), ("k", _p), ("v", _p), ("out", _p), ("attn", _p),
+    ]
+
+
+class AttnMetricArgs(ctypes.Structure):
+    _fields_ = [
+        ("num_query_heads", _i32), ("L", _i32), ("attn", _p), ("mode", _i32), ("window", _i32), ("pool", _i32),
+        ("excluded", _i32), ("aggregation", _i32), ("metrics_out", _p),
+    ]
+
+
 class EvictArgs(ctypes.Structure):
     _fields_ = [
         ("seq_rows", _p), ("budgets", _p), ("n_seqs", _i32), ("max_slots_per_head", _i64),
@@ -107,6 +120,8 @@ _SIGS = {
     "kvc_compress": ([_p, _p, _p], _i32),
     "kvc_full_metric": ([_p, _p, _p], _i32),
     "kvc_prefill_compress": ([_p, _p, _p, _p, _i32, _p], _i32),
+    "kvc_gqa_attention": ([_p, _p, _p], _i32),
+    "kvc_attn_metrics": ([_p, _p, _p], _i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -172,3 +172,63 @@ def accumulate_decode(store: MetricsStore, tables: BlockTables, seq_id: int, lay
     _lib.check(_lib.lib().kvc_accumulate_rows(ctypes.byref(p), row, layer, packed.data_ptr(), r,
                                               packed.shape[-1], cfg.metric_mode, _lib.stream_ptr(dev)),
                "accumulate_decode")
+
+
+# ---------------------------------------------------------------------------
+# reference-signature prompt metrics on an explicit attention tensor
+# ---------------------------------------------------------------------------
+
+
+def _attn_call(attn, cfg: MetricConfig, num_kv_heads: int, mode: int) -> torch.Tensor:
+    dev = _lib.require_cuda(attn.device if torch.is_tensor(attn) and attn.is_cuda else None)
+    a_t = torch.as_tensor(np.asarray(attn) if not torch.is_tensor(attn) else attn).to(dev, torch.float32)
+    a_t = a_t.contiguous()
+    if a_t.dim() != 3 or a_t.shape[1] != a_t.shape[2]:
+        raise ValueError("attn must be (num_query_heads, L, L)")
+    n_q, L = a_t.shape[0], a_t.shape[1]
+    if n_q % num_kv_heads != 0:
+        raise ValueError("query head count not divisible by num_kv_heads")
+    out = torch.empty((num_kv_heads, L), dtype=torch.float32, device=dev)
+    if L == 0:
+        return out
+    a = _lib.AttnMetricArgs()
+    a.num_query_heads, a.L, a.attn, a.mode = n_q, L, a_t.data_ptr(), mode
+    a.window, a.pool, a.excluded, a.aggregation = cfg.window, cfg.pool, cfg.excluded, cfg.metric_mode
+    a.metrics_out = out.data_ptr()
+    p = _lib.KvcPool()
+    p.status = _lib.DeviceContext.get(dev).status.data_ptr()
+    p.num_kv_heads = num_kv_heads
+    from .cache import with_scratch
+    with_scratch(p, dev, num_kv_heads * L * 4 + 256)
+    _lib.check(_lib.lib().kvc_attn_metrics(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)), "attn_metrics")
+    return out
+
+
+def window_metrics(attn, cfg: MetricConfig, num_kv_heads: int):
+    """Observation-window metrics from an (n_q, L, L) causal attention tensor
+    (metrics.py:68-89): f of the last ``cfg.window`` rows summed per key over
+    the key's query group, max-pooled over keys.  Returns (metrics (H, L) fp32
+    device tensor, protected (L,) bool device tensor).  The serving path
+    (prefill_sequence, window_metrics_qk) computes the same from Q and K on
+    tcgen05 without the attention tensor."""
+    out = _attn_call(attn, cfg, num_kv_heads, 0)
+    L = out.shape[1]
+    start = max(L - cfg.window, 0)
+    protected = torch.arange(L, device=out.device) >= start
+    if not cfg.protect_window:
+        protected[:] = False
+    return out, protected
+
+
+def full_metrics(attn, cfg: MetricConfig, num_kv_heads: int) -> torch.Tensor:
+    """Full-range metrics of an attention tensor: key j aggregates query rows
+    i >= j + excluded (metrics.py:92-109).  No pooling, no protection."""
+    return _attn_call(attn, cfg, num_kv_heads, 1)
+
+
+def prompt_metrics(attn, cfg: MetricConfig, num_kv_heads: int):
+    """Dispatch on cfg.mode (metrics.py:112-119): (metrics, protected)."""
+    if cfg.mode == WINDOW:
+        return window_metrics(attn, cfg, num_kv_heads)
+    m = full_metrics(attn, cfg, num_kv_heads)
+    return m, torch.zeros(m.shape[1], dtype=torch.bool, device=m.device)

@@ -74,7 +74,7 @@ def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev,
                "window_metric")
 
 
-def window_metrics(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
+def window_metrics_qk(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
     """Observation-window metrics of one layer from its prompt Q and K.
 
     q: (n_q, L, d) or just the last min(w, L) query rows (n_q, w', d);
@@ -115,7 +115,7 @@ def _full_call(q, k, cfg: MetricConfig, num_kv_heads: int, dev, out) -> None:
     _lib.check(_lib.lib().kvc_full_metric(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)), "full_metric")
 
 
-def full_metrics(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
+def full_metrics_qk(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
     """KVC-full metrics of one layer (metrics.py:92-109): q (n_q, L, d) all
     prompt queries, k (num_kv_heads, L, d).  Returns (metrics (H, L) fp32,
     protected (L,) all False) like prompt_metrics in full mode."""

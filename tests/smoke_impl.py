@@ -58,7 +58,7 @@ def run_smoke():
     got2 = rig2.to_oracle()
     assert np.allclose(got2.metric, st2.metric, rtol=2e-3, atol=1e-6 * st2.metric.max()), "window metric"
     # KVC-full metric (tcgen05 row statistics + column sums)
-    full, _ = K.full_metrics(t(qf[0]), t(kf[0]), K.MetricConfig(mode="full"), H2)
+    full, _ = K.full_metrics_qk(t(qf[0]), t(kf[0]), K.MetricConfig(mode="full"), H2)
     want_full = O.full_metric(qf[0], kf[0], H2, excluded=10, aggregation="L2")
     assert np.allclose(full.cpu().numpy(), want_full, rtol=2e-3, atol=1e-6 * want_full.max()), "full metric"
     print("smoke: decode + compress + window/full metric parity ok")

@@ -210,7 +210,7 @@ def test_full_metric_long(L):
     q = bf16_round(rng.standard_normal((H * r, L, d)))
     k = bf16_round(rng.standard_normal((H, L, d)))
     cfg = K.MetricConfig(mode="full", aggregation="L2", excluded=v)
-    got, _ = K.full_metrics(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), cfg, H)
+    got, _ = K.full_metrics_qk(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), cfg, H)
     _lib.DeviceContext.get(got.device).raise_status()
     want = O.full_metric(q, k, H, v, "L2")
     g = got.cpu().numpy().astype(np.float64)

@@ -36,7 +36,7 @@ def test_full_metric_matches_oracle(H, r, d, L, v, agg):
     q = bf16_round(rng.standard_normal((H * r, L, d)))
     k = bf16_round(rng.standard_normal((H, L, d)))
     cfg = K.MetricConfig(mode="full", aggregation=agg, excluded=v)
-    got, prot = K.full_metrics(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), cfg, H)
+    got, prot = K.full_metrics_qk(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), cfg, H)
     _lib.DeviceContext.get(got.device).raise_status()
     want = O.full_metric(q, k, H, excluded=v, aggregation=agg)
     g = got.cpu().numpy().astype(np.float64)

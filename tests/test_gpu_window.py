@@ -42,7 +42,7 @@ def test_window_metric_matches_oracle(H, r, d, L, window, pool, agg):
     q = bf16_round(rng.standard_normal((H * r, L, d)))
     k = bf16_round(rng.standard_normal((H, L, d)))
     cfg = K.MetricConfig(mode="window", aggregation=agg, window=window, pool=pool)
-    got, prot = K.window_metrics(torch.from_numpy(q[:, L - w:]).cuda(), torch.from_numpy(k).cuda(), cfg, H)
+    got, prot = K.window_metrics_qk(torch.from_numpy(q[:, L - w:]).cuda(), torch.from_numpy(k).cuda(), cfg, H)
     _lib.DeviceContext.get(got.device).raise_status()
     want, wprot = O.window_metric(q[:, L - w:], k, H, window, pool, agg)
     g = got.cpu().numpy().astype(np.float64)

@@ -43,7 +43,8 @@ def test_ctypes_layout_matches_c():
 
     structs = {"kvc_pool": _lib.KvcPool, "kvc_decode_args": _lib.DecodeArgs,
                "kvc_window_args": _lib.WindowArgs, "kvc_evict_args": _lib.EvictArgs,
-               "kvc_full_args": _lib.FullArgs}
+               "kvc_full_args": _lib.FullArgs, "kvc_dense_args": _lib.DenseArgs,
+               "kvc_attn_metric_args": _lib.AttnMetricArgs}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
