@@ -166,16 +166,20 @@ def _prepare(tables: BlockTables, budgets: Mapping[int, int], want_moves: bool, 
     max_slots = min(tables.max_blocks, -(-bound // b) + 1) * b
     nb_bound = max_slots // b
     cap = sum(min(max(r, 0), hp * nb_bound) for r in requested) * b + 1
+    # inputs go up from pinned staging without a host sync; every output
+    # below is written in full by the kernels (K3 writes clamped / evict /
+    # move_offsets, K4 move_counts / evicted_kvs, totals are zeroed in-stream)
+    stage = torch.tensor(rows_host + requested, dtype=torch.int64).pin_memory().to(dev, non_blocking=True)
     plan = EvictionPlan(
         seq_ids=seq_ids, requested=requested,
-        rows=torch.tensor(rows_host, dtype=torch.int32, device=dev),
-        budgets=torch.tensor(requested, dtype=torch.int64, device=dev),
-        clamped=torch.zeros(n, dtype=torch.int64, device=dev),
-        evict=torch.zeros((n, hp), dtype=torch.int32, device=dev),
-        evicted_kvs=torch.zeros((n, hp), dtype=torch.int32, device=dev),
-        move_offsets=torch.zeros(n * hp + 1, dtype=torch.int64, device=dev),
-        move_counts=torch.zeros((n, hp), dtype=torch.int32, device=dev),
-        totals=torch.zeros(4, dtype=torch.int64, device=dev),
+        rows=stage[:n].to(torch.int32),
+        budgets=stage[n:],
+        clamped=torch.empty(n, dtype=torch.int64, device=dev),
+        evict=torch.empty((n, hp), dtype=torch.int32, device=dev),
+        evicted_kvs=torch.empty((n, hp), dtype=torch.int32, device=dev),
+        move_offsets=torch.empty(n * hp + 1, dtype=torch.int64, device=dev),
+        move_counts=torch.empty((n, hp), dtype=torch.int32, device=dev),
+        totals=torch.empty(4, dtype=torch.int64, device=dev),
         moves=torch.empty((cap, 2), dtype=torch.int32, device=dev) if want_moves else None,
         freed=torch.empty((n, hp, tables.max_blocks), dtype=torch.int32, device=dev) if want_freed else None,
         max_slots=max_slots,
@@ -205,7 +209,10 @@ def _scratch_bytes(plan: EvictionPlan, hp: int) -> int:
     n = len(plan.seq_ids)
     T = n * hp
     # keys + per-head counters + per-sequence digit histograms + candidate lists (short heads)
-    return T * ((plan.max_slots + 3) // 4 * 4) * 4 + T * 28 + n * (2048 * 4 + 40) + T * 2 * 256 * 8 + (1 << 16)
+    # + the K/V copy queue (one u64 per 32 moves of capacity, + one per head)
+    cap = plan.moves.shape[0] if plan.moves is not None else 0
+    return (T * ((plan.max_slots + 3) // 4 * 4) * 4 + T * 36 + n * (2048 * 4 + 44) + T * 2 * 256 * 8
+            + (cap // 32 + T + 2) * 8 + (1 << 16))
 
 
 def schedule_evictions(tables: BlockTables, store: MetricsStore, budgets: Mapping[int, int],

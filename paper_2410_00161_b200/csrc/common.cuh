@@ -31,6 +31,11 @@ __host__ __device__ inline int32_t *head_table(const kvc_pool &p, int64_t hidx) 
   return p.tables + hidx * p.max_blocks;
 }
 
+// Programmatic dependent launch: wait for the preceding kernel of the stream
+// (no-op without the launch attribute) / let the next one's CTAs launch.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // First error wins; payload words written by the winner only.
 __device__ inline void set_status(int32_t *status, int code, int32_t a = 0, int32_t b = 0) {
   if (atomicCAS(status, 0, code) == 0) {

@@ -459,10 +459,16 @@ __device__ __forceinline__ void metric_quads(const Params &P, const float *srow,
   for (int g = q_lo + threadIdx.x; g < nq; g += blockDim.x) {
     const int p0 = g * 4;
     float sc[4 * R];
+    if (p0 + 4 <= cp) {
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const float4 v = *reinterpret_cast<const float4 *>(srow + (int64_t)p0 * R + 4 * j);
-      sc[4 * j] = v.x, sc[4 * j + 1] = v.y, sc[4 * j + 2] = v.z, sc[4 * j + 3] = v.w;
+      for (int j = 0; j < R; ++j) {
+        const float4 v = *reinterpret_cast<const float4 *>(srow + (int64_t)p0 * R + 4 * j);
+        sc[4 * j] = v.x, sc[4 * j + 1] = v.y, sc[4 * j + 2] = v.z, sc[4 * j + 3] = v.w;
+      }
+    } else {  // last quad: the scores past cp were never written
+      const int nv = (cp - p0) * R;
+#pragma unroll
+      for (int j = 0; j < 4 * R; ++j) sc[j] = j < nv ? srow[(int64_t)p0 * R + j] : 0.f;
     }
     float c[4];
 #pragma unroll

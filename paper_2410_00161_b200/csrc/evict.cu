@@ -28,12 +28,36 @@
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
+#include <climits>
+#include <utility>
+
 #include "common.cuh"
 
 using namespace kvc;
 
 namespace {
 
+// Launch with programmatic stream serialisation: the kernel's CTAs may start
+// while the previous kernel of the stream drains; every kernel of the chain
+// opens with grid_dep_wait() before touching what its predecessor wrote.
+template <typename... P, typename... A>
+void launch_pdl(void (*fn)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
+}
+
+#ifndef KVC_C16_REGS
+#define KVC_C16_REGS 64  // two 512-thread CTAs per SM
+#endif
 constexpr int kBins = 2048;       // 11-bit digits
 constexpr int kThreads = 512;
 constexpr uint32_t kKeyInf = 0xFF800000u;  // f32_order_key(+inf)
@@ -51,6 +75,19 @@ struct EvictState {
   // per sequence
   int32_t *R;         // [n_seqs][kBins] contribution deltas per digit
   int32_t *done;      // [n_seqs] heads finished in the current histogram kernel (last one finds the digit)
+  int32_t *done_all;  // [1] sequences whose select finished (the last one makes the offsets global)
+  int32_t *kv_ready;  // [T] K/V move list published by the head's compaction CTA: moves + 1 (0 = not yet)
+  int32_t *kv_next;   // [T] next K/V copy chunk of the head to claim
+  int32_t *c16_done;  // [1] k_compact16 CTAs finished (the last one sums the free tiles)
+  // K/V copy queue: each published head appends its 32-move chunks
+  int32_t *pub_count;  // [1] heads published
+  int32_t *chunk_tail; // [1] chunks appended
+  int32_t *claim_next; // [1] next chunk a copier warp takes
+  unsigned long long *chunks;  // [max_chunks] (head + 1) << 32 | chunk of the head; 0 = not yet written
+  int64_t max_chunks;
+  int64_t *totals;    // nullable [4]: zeroed by k_load's first CTA
+  int32_t *zero;      // R .. c16_done: one memset per call
+  int64_t zero_n;
   uint32_t *prefix;   // [n_seqs] T* digits found so far
   int64_t *E;         // [n_seqs] clamped budget (0 = inactive)
   int64_t *seq_moves; // [n_seqs] move slots of the sequence, then its base offset
@@ -67,10 +104,34 @@ __device__ __forceinline__ uint32_t slot_key(const kvc_pool &p, int64_t f, bool 
   return f32_order_key(p.metric[f]);
 }
 
+__device__ __forceinline__ int ld_acquire(const int32_t *a) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
 // Shared-memory histogram increment (same-bin lanes serialise in hardware;
 // warp aggregation with match.any measured slower for metric keys).
 __device__ __forceinline__ void hist_add(int32_t *hist, uint32_t bin, bool active) {
   if (active) atomicAdd(&hist[bin], 1);
+}
+
+// Four consecutive positions of one thread: equal active bins in a row (the
+// pooled metric repeats a window maximum) are added with one atomic.
+__device__ __forceinline__ void hist_add4(int32_t *hist, const uint32_t bin[4], const bool act[4]) {
+  uint32_t cur = 0;
+  int run = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (!act[e]) continue;
+    if (run && bin[e] != cur) {
+      atomicAdd(&hist[cur], run);
+      run = 0;
+    }
+    cur = bin[e];
+    ++run;
+  }
+  if (run) atomicAdd(&hist[cur], run);
 }
 
 // Per-head inclusive scan of a kBins histogram in smem (NT threads,
@@ -192,12 +253,15 @@ __device__ __forceinline__ bool last_of_sequence(EvictState &S, int si) {
 }
 
 // (1) keys + cap + level-1 histogram contributions.
+// Returns true in the CTA that was the sequence's last to arrive (it found
+// the level-1 digit).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
-                                                  EvictState S, int with_hist, int64_t *clamped) {
+__device__ bool load_body(const kvc_pool &p, const int32_t *rows, const int64_t *req, EvictState &S, int with_hist,
+                          int64_t *clamped) {
   __shared__ int32_t hist[kBins];
   __shared__ int32_t shield_s;
   const int g = blockIdx.x;
+  if (g == 0 && threadIdx.x < 4 && S.totals) S.totals[threadIdx.x] = 0;  // the compaction accumulates them
   const int si = g / S.hp, hi = g % S.hp;
   const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
   const int b = p.block_size;
@@ -208,46 +272,82 @@ __global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, co
   uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
   if (n > S.max_slots) {
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_CAPACITY, (int32_t)hidx, (int32_t)n);
-    if (with_hist && last_of_sequence(S, si)) find_digit<NT>(req, S, si, 1, 11, clamped);
-    return;
+    if (with_hist && last_of_sequence(S, si)) {
+      find_digit<NT>(req, S, si, 1, 11, clamped);
+      return true;
+    }
+    return false;
   }
   for (int i = threadIdx.x; i < kBins; i += NT) hist[i] = 0;
   if (threadIdx.x == 0) shield_s = 0;
   __syncthreads();
   int shield = 0;
   if (b == 16) {
-    // one thread per 16-slot block: 64 B metric, 16 B flags, 64 B keys
-    for (int64_t base = 0; base < nb; base += NT) {
-      const int64_t bl = base + threadIdx.x;
-      const bool in = bl < nb;
-      uint32_t kk[16];
-      if (in) {
-        const int64_t f0 = (int64_t)tab[bl] * 16;
+    // one thread per 16-slot block (64 B metric, 16 B flags in, 64 B keys
+    // out); the table entry of the thread's next block is loaded a round
+    // ahead, so each round waits for one load latency, not two
+    constexpr int U = 1;
+    int32_t nxt = threadIdx.x < nb ? tab[threadIdx.x] : -1;
+    for (int64_t base = 0; base < nb; base += NT * U) {
+      int32_t blk[U];
+      blk[0] = nxt;
+      nxt = base + NT + threadIdx.x < nb ? tab[base + NT + threadIdx.x] : -1;
+      float4 mv[U][4];
+      uint4 pr[U], fr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (blk[u] < 0) continue;
+        const int64_t f0 = (int64_t)blk[u] * 16;
         const float4 *mp = reinterpret_cast<const float4 *>(p.metric + f0);
-        const uint4 pr = *reinterpret_cast<const uint4 *>(p.protected_ + f0);
-        const uint4 fr = *reinterpret_cast<const uint4 *>(p.fresh + f0);
-        const uint32_t pw[4] = {pr.x | fr.x, pr.y | fr.y, pr.z | fr.z, pr.w | fr.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mv[u][q] = mp[q];
+        pr[u] = *reinterpret_cast<const uint4 *>(p.protected_ + f0);
+        fr[u] = *reinterpret_cast<const uint4 *>(p.fresh + f0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (blk[u] < 0) continue;
+        const int64_t f0 = (int64_t)blk[u] * 16;
+        const float4 *mp = reinterpret_cast<const float4 *>(p.metric + f0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mv[u][q] = mp[q];
+        pr[u] = *reinterpret_cast<const uint4 *>(p.protected_ + f0);
+        fr[u] = *reinterpret_cast<const uint4 *>(p.fresh + f0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (blk[u] < 0) continue;  // (the block loop's tail: no histogram votes to keep uniform)
+        const int64_t bl = base + u * NT + threadIdx.x;
+        const uint32_t pw[4] = {pr[u].x | fr[u].x, pr[u].y | fr[u].y, pr[u].z | fr[u].z, pr[u].w | fr[u].w};
+        uint4 *kp = reinterpret_cast<uint4 *>(keys + bl * 16);
+        // runs of equal top digits (the pooled metric repeats a window
+        // maximum over neighbouring slots) add to the histogram once per run
+        uint32_t cur = 0xffffffffu;
+        int run = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 mv = mp[q];
-          const float mf[4] = {mv.x, mv.y, mv.z, mv.w};
+          const float mf[4] = {mv[u][q].x, mv[u][q].y, mv[u][q].z, mv[u][q].w};
+          uint32_t kq[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int o = q * 4 + e;
-            const int64_t pos = bl * 16 + o;
+            const int64_t pos = bl * 16 + q * 4 + e;
             const bool occ = pos < C;
             const bool sh = occ && ((pw[q] >> (8 * e)) & 0xff);
             shield += sh ? 1 : 0;
-            kk[o] = !occ ? f32_order_key(0.f) : sh ? kKeyInf : f32_order_key(mf[e]);
+            kq[e] = !occ ? f32_order_key(0.f) : sh ? kKeyInf : f32_order_key(mf[e]);
+            if (with_hist) {
+              const uint32_t bin = kq[e] >> 21;
+              if (bin != cur) {
+                if (run) atomicAdd(&hist[cur], run);
+                cur = bin;
+                run = 0;
+              }
+              ++run;
+            }
           }
+          kp[q] = make_uint4(kq[0], kq[1], kq[2], kq[3]);
         }
-        uint4 *kp = reinterpret_cast<uint4 *>(keys + bl * 16);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) kp[q] = make_uint4(kk[4 * q], kk[4 * q + 1], kk[4 * q + 2], kk[4 * q + 3]);
-      }
-      if (with_hist) {
-#pragma unroll
-        for (int o = 0; o < 16; ++o) hist_add(hist, in ? kk[o] >> 21 : 0, in);
+        if (with_hist && run) atomicAdd(&hist[cur], run);
       }
     }
   } else {
@@ -272,24 +372,33 @@ __global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, co
   int cap = nb - (sh_blocks > 1 ? sh_blocks : 1);
   if (cap < 0) cap = 0;
   if (threadIdx.x == 0) S.cap[g] = cap;
-  if (!with_hist) return;
+  if (!with_hist) return false;
   if (req[si] > 0) {
     scan_hist<NT>(hist);
     add_contrib<NT>(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
   }
-  if (last_of_sequence(S, si)) find_digit<NT>(req, S, si, 1, 11, clamped);
+  if (!last_of_sequence(S, si)) return false;
+  find_digit<NT>(req, S, si, 1, 11, clamped);
+  return true;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
+                                                  EvictState S, int with_hist, int64_t *clamped) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  load_body<NT>(p, rows, req, S, with_hist, clamped);
 }
 
 // (3/5) per head: histogram of the next digit among keys matching the prefix.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
-                                                  int shift, int bits, const int64_t *req, int level,
-                                                  int64_t *clamped) {
+__device__ bool hist_body(const kvc_pool &p, const int32_t *rows, EvictState &S, int shift_hi, int shift, int bits,
+                          const int64_t *req, int level, int64_t *clamped) {
   __shared__ int32_t hist[kBins];
   __shared__ int64_t below_s;
   const int g = blockIdx.x;
   const int si = g / S.hp, hi = g % S.hp;
-  if (S.E[si] <= 0) return;
+  if (S.E[si] <= 0) return false;
   const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
   const int b = p.block_size;
   const int64_t n = (int64_t)p.nblocks[hidx] * b;
@@ -310,13 +419,17 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
       uint4 k4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
       if (pos < n) k4 = *reinterpret_cast<const uint4 *>(keys + pos);
       const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+      uint32_t bin[4];
+      bool act[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const bool in = pos + e < n;
         const uint32_t top = kv[e] >> shift_hi;
         below += (in && top < pre) ? 1 : 0;
-        hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
+        bin[e] = (kv[e] >> shift) & dmask;
+        act[e] = in && top == pre;
       }
+      hist_add4(hist, bin, act);
     }
   } else {
     for (int64_t base = 0; base < n; base += 4 * NT * U) {
@@ -331,13 +444,17 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
       for (int u = 0; u < U; ++u) {
         const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);
         const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+        uint32_t bin[4];
+        bool act[4];
   #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const bool in = pos + e < n;
           const uint32_t top = kv[e] >> shift_hi;
           below += (in && top < pre) ? 1 : 0;
-          hist_add(hist, (kv[e] >> shift) & dmask, in && top == pre);
+          bin[e] = (kv[e] >> shift) & dmask;
+          act[e] = in && top == pre;
         }
+        hist_add4(hist, bin, act);
       }
     }
   }
@@ -346,23 +463,68 @@ __global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, Ev
   __syncthreads();
   scan_hist<NT>(hist);
   add_contrib<NT>(hist, (int32_t)below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
-  if (last_of_sequence(S, si)) find_digit<NT>(req, S, si, level, bits, clamped);
+  if (!last_of_sequence(S, si)) return false;
+  find_digit<NT>(req, S, si, level, bits, clamped);
+  return true;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
+                                                  int shift, int bits, const int64_t *req, int level,
+                                                  int64_t *clamped) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  hist_body<NT>(p, rows, S, shift_hi, shift, bits, req, level, clamped);
 }
 
 // (7) per head: rows with threshold < T* and <= T*.  With S.cand, also the
 // composites (key << 32 | secondary) of the keys < T* and of the ties at T*
 // (first kCand of each, any order) for k_compact_warp.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, EvictState S) {
+__device__ void bounds_counts(const kvc_pool &p, const int32_t *rows, EvictState &S, int g, int si, int hi);
+template <int NT>
+__device__ void select_seq(EvictState &S, int si, int bsz, int32_t *evict, int64_t *move_off, int32_t *status);
+template <int NT>
+__device__ void offsets_all(EvictState &S, int n_seqs, int64_t *move_off);
+
+// (7-8) per head: rows with threshold < T* and <= T*; then the last CTA of
+// each sequence takes the tie rows in head order (e_h) and the last sequence
+// makes the move offsets global.
+template <int NT>
+__device__ void bounds_body(const kvc_pool &p, const int32_t *rows, EvictState &S, int n_seqs, int bsz,
+                            int32_t *evict, int64_t *move_off) {
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  if (S.E[si] > 0) bounds_counts<NT>(p, rows, S, g, si, hi);
+  else if (threadIdx.x == 0) { S.lo[g] = 0; S.hi[g] = 0; }
+  if (!last_of_sequence(S, si)) return;
+  select_seq<NT>(S, si, bsz, evict, move_off, p.status);
+  __shared__ int last_all;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(S.done_all) : "memory");
+    last_all = prev == n_seqs - 1;
+    if (last_all) *S.done_all = 0;
+  }
+  __syncthreads();
+  if (last_all) offsets_all<NT>(S, n_seqs, move_off);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, EvictState S, int n_seqs, int bsz,
+                                                    int32_t *evict, int64_t *move_off) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  bounds_body<NT>(p, rows, S, n_seqs, bsz, evict, move_off);
+}
+
+
+template <int NT>
+__device__ void bounds_counts(const kvc_pool &p, const int32_t *rows, EvictState &S, int g, int si, int hi) {
   using Red = cub::BlockReduce<int32_t, NT>;
   __shared__ typename Red::TempStorage tmp;
   __shared__ int32_t cnt_s[2];
-  const int g = blockIdx.x;
-  const int si = g / S.hp, hi = g % S.hp;
-  if (S.E[si] <= 0) {
-    if (threadIdx.x == 0) { S.lo[g] = 0; S.hi[g] = 0; }
-    return;
-  }
   const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
   const int b = p.block_size;
   const int64_t n = (int64_t)p.nblocks[hidx] * b;
@@ -470,31 +632,34 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   }
 }
 
-// (8) one CTA per sequence: e_h = L_h + ties taken in head order, and the
-// sequence-local exclusive offsets of e_h*b (made global by k_offsets).
-__global__ void __launch_bounds__(1024) k_select(EvictState S, int bsz, int32_t *evict, int64_t *move_off,
-                                                int32_t *status) {
-  using Scan = cub::BlockScan<int64_t, 1024>;
-  using Red = cub::BlockReduce<int64_t, 1024>;
+// (8) last CTA of a sequence: e_h = L_h + ties taken in head order, and the
+// sequence-local exclusive offsets of e_h*b (made global by offsets_all).
+// Other CTAs' counts are read through L2 (acquired by the arrival).
+template <int NT>
+__device__ void select_seq(EvictState &S, int si, int bsz, int32_t *evict, int64_t *move_off, int32_t *status) {
+  using Scan = cub::BlockScan<int64_t, NT>;
+  using Red = cub::BlockReduce<int64_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ typename Red::TempStorage rtmp;
   __shared__ int64_t less_s;
   const int hp = S.hp;
-  const int si = blockIdx.x;
   const int64_t E = S.E[si];
   // total rows strictly below T*
   int64_t less = 0;
-  for (int h = threadIdx.x; h < hp; h += 1024) less += E > 0 ? S.lo[(int64_t)si * hp + h] : 0;
+  for (int h = threadIdx.x; h < hp; h += NT) less += E > 0 ? __ldcg(S.lo + (int64_t)si * hp + h) : 0;
   less = Red(rtmp).Sum(less);
   if (threadIdx.x == 0) less_s = less;
   __syncthreads();
   const int64_t need = E - less_s;  // tie rows to take at T*, in head order
   int64_t tcarry = 0, ocarry = 0;
-  for (int base = 0; base < hp; base += 1024) {
+  for (int base = 0; base < hp; base += NT) {
     const int h = base + threadIdx.x;
     const int64_t g = (int64_t)si * hp + h;
-    int64_t ties = 0;
-    if (h < hp && E > 0) ties = S.hi[g] - S.lo[g];
+    int64_t ties = 0, lo = 0;
+    if (h < hp && E > 0) {
+      lo = __ldcg(S.lo + g);
+      ties = __ldcg(S.hi + g) - lo;
+    }
     int64_t excl, tot;
     Scan(tmp).ExclusiveSum(ties, excl, tot);
     int32_t eh = 0;
@@ -502,7 +667,7 @@ __global__ void __launch_bounds__(1024) k_select(EvictState S, int bsz, int32_t 
       int64_t take = need - (tcarry + excl);
       if (take < 0) take = 0;
       if (take > ties) take = ties;
-      eh = E > 0 ? (int32_t)(S.lo[g] + take) : 0;
+      eh = E > 0 ? (int32_t)(lo + take) : 0;
       evict[g] = eh;
     }
     __syncthreads();
@@ -519,16 +684,22 @@ __global__ void __launch_bounds__(1024) k_select(EvictState S, int bsz, int32_t 
   }
 }
 
-// (8b) one CTA: sequence bases -> global exclusive offsets over all heads.
-__global__ void __launch_bounds__(1024) k_offsets(EvictState S, int n_seqs, int64_t *move_off) {
-  using Scan = cub::BlockScan<int64_t, 1024>;
+// (8b) last sequence: sequence bases -> global exclusive offsets over all heads.
+template <int NT>
+__device__ void offsets_all(EvictState &S, int n_seqs, int64_t *move_off) {
+  using Scan = cub::BlockScan<int64_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int base = 0; base < n_seqs; base += 1024) {
+  const int64_t T = (int64_t)n_seqs * S.hp;
+  if (n_seqs == 1) {  // offsets are already global
+    if (threadIdx.x == 0) move_off[T] = __ldcg(S.seq_moves);
+    return;
+  }
+  for (int base = 0; base < n_seqs; base += NT) {
     const int si = base + threadIdx.x;
-    const int64_t v = si < n_seqs ? S.seq_moves[si] : 0;
+    const int64_t v = si < n_seqs ? __ldcg(S.seq_moves + si) : 0;
     int64_t excl, tot;
     Scan(tmp).ExclusiveSum(v, excl, tot);
     if (si < n_seqs) S.seq_moves[si] = carry + excl;  // now the sequence base
@@ -536,8 +707,7 @@ __global__ void __launch_bounds__(1024) k_offsets(EvictState S, int n_seqs, int6
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  const int64_t T = (int64_t)n_seqs * S.hp;
-  for (int64_t g = threadIdx.x; g < T; g += 1024) move_off[g] += S.seq_moves[g / S.hp];
+  for (int64_t g = threadIdx.x; g < T; g += NT) move_off[g] = __ldcg(move_off + g) + S.seq_moves[g / S.hp];
   if (threadIdx.x == 0) move_off[T] = carry;
 }
 
@@ -593,11 +763,201 @@ struct MoveArgs {
   int64_t *totals;
   int32_t *src_pos;     // nullable [T][max_slots]: pre-renumbering logical of each kept position
   int64_t src_stride;
+  int publish;          // k_compact16 publishes each head's move list for k_copy_published
+  int64_t n_heads;      // T
 };
+
+// Named barrier over `count` threads (a warp-aligned group of the CTA).
+// (ids 1 and 2 only, as immediates, so ptxas reserves three barriers)
+__device__ __forceinline__ void group_sync(int id, int count) {
+  if (id == 1) asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory");
+  else asm volatile("bar.sync 2, %0;" ::"r"(count) : "memory");
+}
+
+// Exclusive scan over a warp-aligned group of GT threads (gtid = rank in the
+// group); wsum = 32 ints of shared memory owned by the group.
+__device__ __forceinline__ int32_t group_excl_scan(int32_t v, int gtid, int GT, int bar, int32_t *wsum,
+                                                   int32_t &total) {
+  const int lane = gtid & 31, w = gtid >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  group_sync(bar, GT);
+  int32_t pre = 0, tot = 0;
+  for (int i = 0; i < GT / 32; ++i) {
+    const int32_t t = wsum[i];
+    pre += i < w ? t : 0;
+    tot += t;
+  }
+  group_sync(bar, GT);
+  total = tot;
+  return pre + x - v;
+}
+
+constexpr int kKvChunk = 32;  // moves per claim: one per lane of the claiming warp
+
+// Copier warps of k_compact16: claim 32-move chunks of head h's move list
+// until none are left (claims are atomic, so the owner CTA's warps and
+// helpers never overlap).  Each lane holds one move's (src, dst); the warp
+// then streams the K and V rows of the chunk's moves, 16-byte units per lane,
+// U units in flight.  Sources sit in blocks this round frees: read once,
+// streamed.
+__device__ void kv_drain(const kvc_pool &p, const EvictState &S, const MoveArgs &M, int64_t h, int nm) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const int vec = p.head_dim / 8, cm = 2 * vec;  // 16-byte units per move (K row, then V row)
+  uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
+  uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
+  const int2 *mv = reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h);
+  const int nch = (nm + kKvChunk - 1) / kKvChunk;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&S.kv_next[h], 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= nch) break;
+    const int k0 = c * kKvChunk;
+    const int cnt = nm - k0 < kKvChunk ? nm - k0 : kKvChunk;
+    int2 sd = make_int2(0, 0);
+    if (lane < cnt) sd = __ldcg(mv + k0 + lane);
+    const int units = cnt * cm;
+    for (int b = 0; b < units; b += 32 * U) {
+      uint4 val[U];
+      uint4 *dst[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const int u = b + i * 32 + lane;
+        const int j = u / cm;  // move of this unit (lanes past the chunk read lane j's pair harmlessly)
+        const int src = __shfl_sync(0xffffffffu, sd.x, j & 31);
+        const int dd = __shfl_sync(0xffffffffu, sd.y, j & 31);
+        dst[i] = nullptr;
+        if (u < units) {
+          int cc = u - j * cm;
+          uint4 *base = cc >= vec ? vc : kc;
+          cc -= cc >= vec ? vec : 0;
+          val[i] = __ldcs(base + (int64_t)src * vec + cc);
+          dst[i] = base + (int64_t)dd * vec + cc;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+        if (dst[i]) *dst[i] = val[i];
+    }
+  }
+}
+
+
+// k_compact16 (whole CTA): head h's move list (nm moves) is complete; append
+// its 32-move chunks to the copy queue (the list is released before the
+// chunk entries, the entries before the head counts as published).
+template <int NT>
+__device__ void publish_moves(const EvictState &S, int64_t h, int nm) {
+  __shared__ int base_s;
+  const int nch = (nm + 31) / 32;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(S.kv_ready + h), "r"(nm + 1) : "memory");
+    base_s = nch ? atomicAdd(S.chunk_tail, nch) : 0;
+  }
+  __syncthreads();
+  __threadfence();
+  for (int c = threadIdx.x; c < nch; c += NT) {
+    const unsigned long long v = ((unsigned long long)(h + 1) << 32) | (unsigned)c;
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(S.chunks + base_s + c), "l"(v) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(S.pub_count) : "memory");
+  }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+
+// K/V rows of every move of the round, running beside k_compact16 (launched
+// programmatically: its CTAs take the SMs compact16's CTAs leave).  A warp
+// claims queue chunks one at a time (32 moves, one (src, dst) per lane).  All
+// compact16 CTAs are resident by the time this grid launches (they trigger
+// first) and every one of them publishes (0 moves when it evicts nothing), so
+// waiting for a chunk entry cannot deadlock; a bounded wait still turns a
+// missing publication into a status error instead of a hang.  The final
+// griddepcontrol.wait makes this grid's completion imply compact16's.
+template <int U>
+__global__ void __launch_bounds__(256) k_copy_published(kvc_pool p, EvictState S, MoveArgs M) {
+  const int lane = threadIdx.x & 31;
+  const int T = (int)M.n_heads;
+  const int vec = p.head_dim / 8, cm = 2 * vec;  // 16-byte units per move (K row, then V row)
+  uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
+  uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
+  unsigned long long t0 = 0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long d = 0;
+    if (lane == 0) {
+      const int id = atomicAdd(S.claim_next, 1);
+      for (int spin = 0;; ++spin) {
+        d = id < S.max_chunks ? ld_acquire64(S.chunks + id) : 0;
+        if (d) break;
+        if (ld_acquire(S.pub_count) == T && id >= __ldcg(S.chunk_tail)) break;  // all published, no more work
+        if ((spin & 63) == 63) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+          if (t - t0 > 2000000000ull) {  // 2 s: a head never published
+            set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, -1, id);
+            break;
+          }
+        }
+        __nanosleep(128);
+      }
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (!d) break;
+    const int64_t h = (int64_t)(d >> 32) - 1;
+    const int k0 = (int)(d & 0xffffffffu) * 32;
+    const int nm = __ldcg(S.kv_ready + h) - 1;  // released before the chunk entry
+    const int cnt = nm - k0 < 32 ? nm - k0 : 32;
+    const int2 *mv = reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h) + k0;
+    int2 sd = make_int2(0, 0);
+    if (lane < cnt) sd = __ldcg(mv + lane);
+    const int units = cnt * cm;
+    for (int b = 0; b < units; b += 32 * U) {
+      uint4 val[U];
+      uint4 *dst[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const int u = b + i * 32 + lane;
+        const int j = u / cm;
+        const int src = __shfl_sync(0xffffffffu, sd.x, j & 31);
+        const int dd = __shfl_sync(0xffffffffu, sd.y, j & 31);
+        dst[i] = nullptr;
+        if (u < units) {
+          int c = u - j * cm;
+          uint4 *base = c >= vec ? vc : kc;
+          c -= c >= vec ? vec : 0;
+          val[i] = __ldcs(base + (int64_t)src * vec + c);
+          dst[i] = base + (int64_t)dd * vec + c;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+        if (dst[i]) *dst[i] = val[i];
+    }
+  }
+  grid_dep_wait();
+}
 
 // (9) per head with e > 0: mask, MoveCache pairing, copies, free, renumber.
 __global__ void __launch_bounds__(kThreads) k_compact(kvc_pool p, const int32_t *rows, EvictState S,
                                                      MoveArgs M) {
+  grid_dep_wait();
+  grid_dep_trigger();
   extern __shared__ uint32_t bitmap[];  // max_slots bits
   __shared__ int32_t hist[kBins];
   __shared__ int32_t cnt_s[4];
@@ -821,11 +1181,14 @@ __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, 
       uint32_t v[4] = {0u, 0u, 0u, 0u};
       bool ok[4] = {false, false, false, false};
       if (q * 4 < n) get4(q * 4, v, ok);
+      uint32_t bin[4];
+      bool act[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const bool m = ok[e] && (shift_hi >= 32 || (v[e] >> shift_hi) == pre);
-        hist_add(hist, (v[e] >> shift) & dmask, m);
+        act[e] = ok[e] && (shift_hi >= 32 || (v[e] >> shift_hi) == pre);
+        bin[e] = (v[e] >> shift) & dmask;
       }
+      hist_add4(hist, bin, act);
     }
     __syncthreads();
     scan_hist16<NT>(hist);
@@ -849,8 +1212,41 @@ __device__ uint32_t select16(int32_t *hist, int64_t n, int64_t rank, Get4 get4, 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
+__device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, const MoveArgs &M, uint32_t *bitmap);
+
+// Last CTA of the grid to arrive: free-block total over the tiles (after every
+// CTA's free-tile atomics, acquired by the arrival).
+template <int NT>
+__device__ void free_total_last(const kvc_pool &p, int32_t *done, int64_t *totals) {
+  __shared__ int last_s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(done) : "memory");
+    last_s = prev == (int)gridDim.x - 1;
+    if (last_s) *done = 0;
+  }
+  __syncthreads();
+  if (!last_s) return;
+  using Red = cub::BlockReduce<int64_t, NT>;
+  __shared__ typename Red::TempStorage tmp;
+  int64_t s = 0;
+  for (int t = threadIdx.x; t < num_tiles(&p); t += NT) s += __ldcg(p.free_tile + t);
+  s = Red(tmp).Sum(s);
+  if (threadIdx.x == 0) totals[3] = s;
+}
+
+template <int NT>
+__global__ void __maxnreg__(KVC_C16_REGS) k_compact16(kvc_pool p, const int32_t *rows, EvictState S, MoveArgs M) {
+  grid_dep_wait();
+  grid_dep_trigger();
   extern __shared__ uint32_t bitmap[];  // [words] bitmap + [words] prefix
+  compact16_head<NT>(p, rows, S, M, bitmap);
+  if (M.totals) free_total_last<NT>(p, S.c16_done, M.totals);
+}
+
+template <int NT>
+__device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, const MoveArgs &M, uint32_t *bitmap) {
   __shared__ int32_t hist[kBins];
   __shared__ int32_t cnt_s[4];
   using Scan = cub::BlockScan<int32_t, NT>;
@@ -860,7 +1256,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
   const int e = M.evict[g];
   if (threadIdx.x == 0 && M.move_counts) M.move_counts[g] = 0;
   if (threadIdx.x == 0 && M.evicted_kvs) M.evicted_kvs[g] = 0;
-  if (e <= 0) return;
+  if (e <= 0) {
+    if (M.publish) publish_moves<NT>(S, g, 0);
+    return;
+  }
   const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
   const int nb = p.nblocks[hidx];
   const int C = p.ctx[hidx];
@@ -1060,131 +1459,141 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_compact16(kvc_pool p, const i
   const int32_t nmoves = cnt_s[1];
   if (nmoves > cnt_s[0]) {
     if (threadIdx.x == 0) set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, (int32_t)hidx, nmoves);
+    if (M.publish) publish_moves<NT>(S, g, 0);
     return;
   }
   if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 3] = t_; }
-  for (int k0 = threadIdx.x; k0 < nmoves; k0 += 4 * NT) {  // four moves' loads in flight per thread
-    int64_t src[4], dst[4];
-    float mt[4];
-    int32_t lg[4];
-    uint8_t pr[4], fr[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + u * NT;
-      src[u] = k < nmoves ? mv[2 * k] : -1;
-      dst[u] = k < nmoves ? mv[2 * k + 1] : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (src[u] >= 0) {
-        mt[u] = p.metric[src[u]];
-        lg[u] = p.logical[src[u]];
-        pr[u] = p.protected_[src[u]];
-        fr[u] = p.fresh[src[u]];
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (src[u] >= 0) {
-        p.metric[dst[u]] = mt[u];
-        p.logical[dst[u]] = lg[u];
-        p.protected_[dst[u]] = pr[u];
-        p.fresh[dst[u]] = fr[u];
-      }
-  }
-  __syncthreads();
-  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 4] = t_; }
-  // ---- free the trailing e blocks and reset their slots ----
-  for (int t = threadIdx.x; t < e; t += NT) {
-    const int j = rb + t;
-    const int32_t blk = tab[j];
-    const int64_t f0 = (int64_t)blk * 16;
-    float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
-    int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      lp[q] = make_int4(-1, -1, -1, -1);
-    }
-    *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
-    p.free_flag[blk] = 1;
-    if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
-  }
-  {
-    // free-tile counts: one atomic per (warp, tile) instead of per block
-    // (a head's blocks sit in a few tiles, so per-block atomics serialise)
-    for (int base = 0; base < e; base += NT) {
-      const int t = base + threadIdx.x;
-      const bool act = t < e;
-      const unsigned am = __ballot_sync(0xffffffffu, act);
-      if (act) {
-        const int tile = tab[rb + t] / KVC_FREE_TILE;
-        const unsigned peers = __match_any_sync(am, tile);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&p.free_tile[tile], __popc(peers));
-      }
-    }
-  }
+  // the move list is complete: the concurrent copy kernel can take it
+  if (M.publish) publish_moves<NT>(S, g, nmoves);
+  constexpr int GT = NT;
+  const int gtid = threadIdx.x;
+  constexpr int bar = 1;
+  __shared__ int32_t wsum_s[32];
   const int keep = rb;
   const int Cn = C < keep * 16 ? C : keep * 16;
-  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 5] = t_; }
-  // ---- logical renumbering: rank among the kept logicals ----
-  const int words = (int)((n + 31) / 32);
-  uint32_t *wpre = bitmap + words;
-  for (int w = threadIdx.x; w < words; w += NT) bitmap[w] = 0;
-  __syncthreads();
-  const int kb = (Cn + 15) / 16;
-  for (int bl = threadIdx.x; bl < kb; bl += NT) {
-    const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int4 l4 = lp[q];
-      const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int pos = bl * 16 + q * 4 + i;
-        if (pos >= Cn) continue;
-        const int32_t lg = lv[i];
-        if (lg < 0 || lg >= n) {
-          set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
-          continue;
-        }
-        const uint32_t bit = 1u << (lg & 31);
-        if (atomicOr(&bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
-      }
-    }
-  }
-  __syncthreads();
   {
-    int32_t carry = 0;
-    for (int base = 0; base < words; base += NT) {
-      const int w = base + threadIdx.x;
-      const int32_t c = w < words ? __popc(bitmap[w]) : 0;
-      int32_t excl, tot;
-      Scan(stmp).ExclusiveSum(c, excl, tot);
-      if (w < words) wpre[w] = carry + excl;
-      carry += tot;
-      __syncthreads();
+    for (int k0 = gtid; k0 < nmoves; k0 += 4 * GT) {  // four moves' loads in flight per thread
+      int64_t src[4], dst[4];
+      float mt[4];
+      int32_t lg[4];
+      uint8_t pr[4], fr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * GT;
+        src[u] = k < nmoves ? mv[2 * k] : -1;
+        dst[u] = k < nmoves ? mv[2 * k + 1] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (src[u] >= 0) {
+          mt[u] = p.metric[src[u]];
+          lg[u] = p.logical[src[u]];
+          pr[u] = p.protected_[src[u]];
+          fr[u] = p.fresh[src[u]];
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (src[u] >= 0) {
+          p.metric[dst[u]] = mt[u];
+          p.logical[dst[u]] = lg[u];
+          p.protected_[dst[u]] = pr[u];
+          p.fresh[dst[u]] = fr[u];
+        }
     }
+    group_sync(bar, GT);
+    if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 4] = t_; }
+    // ---- free the trailing e blocks and reset their slots ----
+    for (int t = gtid; t < e; t += GT) {
+      const int j = rb + t;
+      const int32_t blk = tab[j];
+      const int64_t f0 = (int64_t)blk * 16;
+      float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
+      int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        lp[q] = make_int4(-1, -1, -1, -1);
+      }
+      *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
+      p.free_flag[blk] = 1;
+      if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
+    }
+    {
+      // free-tile counts: one atomic per (warp, tile) instead of per block
+      // (a head's blocks sit in a few tiles, so per-block atomics serialise)
+      for (int base = 0; base < e; base += GT) {
+        const int t = base + gtid;
+        const bool act = t < e;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          const int tile = tab[rb + t] / KVC_FREE_TILE;
+          const unsigned peers = __match_any_sync(am, tile);
+          if ((gtid & 31) == __ffs(peers) - 1) atomicAdd(&p.free_tile[tile], __popc(peers));
+        }
+      }
+    }
+    if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 5] = t_; }
+    // ---- logical renumbering: rank among the kept logicals ----
+    const int words = (int)((n + 31) / 32);
+    uint32_t *wpre = bitmap + words;
+    for (int w = gtid; w < words; w += GT) bitmap[w] = 0;
+    group_sync(bar, GT);
+    const int kb = (Cn + 15) / 16;
+    for (int bl = gtid; bl < kb; bl += GT) {
+      const int4 *lp = reinterpret_cast<const int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 l4 = lp[q];
+        const int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int pos = bl * 16 + q * 4 + i;
+          if (pos >= Cn) continue;
+          const int32_t lg = lv[i];
+          if (lg < 0 || lg >= n) {
+            set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+            continue;
+          }
+          const uint32_t bit = 1u << (lg & 31);
+          if (atomicOr(&bitmap[lg >> 5], bit) & bit) set_status(p.status, KVC_DEV_CACHE_CORRUPTION, (int32_t)hidx, lg);
+        }
+      }
+    }
+    group_sync(bar, GT);
+    {
+      int32_t carry = 0;
+      for (int base = 0; base < words; base += GT) {
+        const int w = base + gtid;
+        const int32_t c = w < words ? __popc(bitmap[w]) : 0;
+        int32_t tot;
+        const int32_t excl = group_excl_scan(c, gtid, GT, bar, wsum_s, tot);
+        if (w < words) wpre[w] = carry + excl;
+        carry += tot;
+      }
+    }
+    group_sync(bar, GT);
+    for (int bl = gtid; bl < kb; bl += GT) {
+      int4 *lp = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int4 l4 = lp[q];
+        int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int pos = bl * 16 + q * 4 + i;
+          const int32_t lg = lv[i];
+          if (M.src_pos && pos < Cn) M.src_pos[g * M.src_stride + pos] = (lg < 0 || lg >= n) ? -1 : lg;
+          if (pos >= Cn || lg < 0 || lg >= n) continue;
+          lv[i] = (int32_t)wpre[lg >> 5] + __popc(bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
+        }
+        lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+      }
+    }
+    if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 6] = t_; }
   }
   __syncthreads();
-  for (int bl = threadIdx.x; bl < kb; bl += NT) {
-    int4 *lp = reinterpret_cast<int4 *>(p.logical + (int64_t)tab[bl] * 16);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int4 l4 = lp[q];
-      int32_t lv[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int pos = bl * 16 + q * 4 + i;
-        const int32_t lg = lv[i];
-        if (M.src_pos && pos < Cn) M.src_pos[g * M.src_stride + pos] = (lg < 0 || lg >= n) ? -1 : lg;
-        if (pos >= Cn || lg < 0 || lg >= n) continue;
-        lv[i] = (int32_t)wpre[lg >> 5] + __popc(bitmap[lg >> 5] & ((1u << (lg & 31)) - 1u));
-      }
-      lp[q] = make_int4(lv[0], lv[1], lv[2], lv[3]);
-    }
-  }
-  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 6] = t_; }
+  if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 7] = t_; }
   if (threadIdx.x == 0) {
     p.nblocks[hidx] = keep;
     p.ctx[hidx] = Cn;
@@ -1302,6 +1711,8 @@ __device__ void warp_sort(unsigned long long *a, int cnt, int lane) {
 
 __global__ void __launch_bounds__(kWC * 32, 4) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
                                                           MoveArgs M, int64_t T_heads) {
+  grid_dep_wait();
+  grid_dep_trigger();
   __shared__ WarpArea area[kWC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * kWC + warp;
@@ -1655,6 +2066,8 @@ __device__ __forceinline__ void copy_rows(Chunk *kc, Chunk *vc, const int64_t *s
 
 __global__ void __launch_bounds__(256) k_copy_kv(kvc_pool p, const int32_t *moves, const int64_t *move_off,
                                                 const int32_t *move_counts, int64_t T) {
+  grid_dep_wait();
+  grid_dep_trigger();
   __shared__ int64_t s_src[8][32], s_dst[8][32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t cap = move_off[T];
@@ -1697,6 +2110,8 @@ __global__ void __launch_bounds__(256) k_copy_kv(kvc_pool p, const int32_t *move
 // this kernel completes (stream order).
 __global__ void __launch_bounds__(256) k_copy_kv_heads(kvc_pool p, const int32_t *moves, const int64_t *move_off,
                                                 const int32_t *move_counts) {
+  grid_dep_wait();
+  grid_dep_trigger();
   const int g = blockIdx.x;
   const int n = move_counts[g];
   if (n == 0) return;
@@ -1772,6 +2187,8 @@ __global__ void __launch_bounds__(256) k_place_prompt_kv(kvc_pool p, const int32
                                                          const int32_t *evict, const int32_t *src_pos,
                                                          int64_t src_stride, const uint4 *k, const uint4 *v,
                                                          int L) {
+  grid_dep_wait();
+  grid_dep_trigger();
   const int g = blockIdx.x;
   const int si = g / hp, hi = g % hp;
   const int64_t hidx = (int64_t)rows[si] * hp + hi;
@@ -1816,6 +2233,8 @@ __global__ void __launch_bounds__(256) k_place_prompt_kv(kvc_pool p, const int32
 }
 
 __global__ void k_free_total(kvc_pool p, int64_t *totals) {
+  grid_dep_wait();
+  grid_dep_trigger();
   using Red = cub::BlockReduce<int64_t, 1024>;
   __shared__ typename Red::TempStorage tmp;
   int64_t s = 0;
@@ -1843,8 +2262,24 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.lec = sc.take<int32_t>(T);
   S.lt1 = sc.take<int32_t>(T);
   S.lt2 = sc.take<int32_t>(T);
-  S.R = sc.take<int32_t>((int64_t)a->n_seqs * kBins);
-  S.done = sc.take<int32_t>(a->n_seqs);
+  // zero-initialised block: digit deltas, arrival counters, K/V copy claims
+  S.zero_n = (int64_t)a->n_seqs * kBins + a->n_seqs + 1 + 2 * T + 1 + 3;
+  S.max_chunks = a->moves_capacity / 32 + T + 1;
+  S.zero_n += 2 * S.max_chunks + 1;  // the chunk queue (u64, 8-byte aligned below)
+  S.zero = sc.take<int32_t>(S.zero_n);
+  S.R = S.zero;
+  S.done = S.zero ? S.R + (int64_t)a->n_seqs * kBins : nullptr;
+  S.done_all = S.zero ? S.done + a->n_seqs : nullptr;
+  S.kv_ready = S.zero ? S.done_all + 1 : nullptr;
+  S.kv_next = S.zero ? S.kv_ready + T : nullptr;
+  S.c16_done = S.zero ? S.kv_next + T : nullptr;
+  S.pub_count = S.zero ? S.c16_done + 1 : nullptr;
+  S.chunk_tail = S.zero ? S.pub_count + 1 : nullptr;
+  S.claim_next = S.zero ? S.chunk_tail + 1 : nullptr;
+  S.chunks = S.zero ? reinterpret_cast<unsigned long long *>(
+                          (reinterpret_cast<uintptr_t>(S.claim_next + 1) + 7) & ~uintptr_t(7))
+                    : nullptr;
+  S.totals = a->totals;
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
   S.seq_moves = sc.take<int64_t>(a->n_seqs);
@@ -1866,52 +2301,184 @@ int validate(const kvc_pool *pool, const kvc_evict_args *a) {
 
 int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s) {
   const int64_t T = (int64_t)a->n_seqs * S.hp;
-  cudaMemsetAsync(S.R, 0, (int64_t)a->n_seqs * kBins * sizeof(int32_t), s);
-  cudaMemsetAsync(S.done, 0, (int64_t)a->n_seqs * sizeof(int32_t), s);
+  cudaMemsetAsync(S.zero, 0, S.zero_n * sizeof(int32_t), s);
   // three radix levels (11 + 11 + 10 bits); the last head CTA of each
-  // sequence finds that level's digit inside the histogram kernel
+  // sequence finds that level's digit inside the histogram kernel; the last
+  // one of k_bounds selects the tie rows and the move offsets
   if (small_heads(S)) {
     constexpr int NT = 256;
-    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3, a->clamped);
-    k_bounds<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S);
+    launch_pdl(k_load<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, a->budgets, S, 1, a->clamped);
+    launch_pdl(k_hist<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2,
+               a->clamped);
+    launch_pdl(k_hist<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3,
+               a->clamped);
+    launch_pdl(k_bounds<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, a->n_seqs, pool->block_size,
+               a->evict, a->move_offsets);
   } else {
     constexpr int NT = kThreads;
-    k_load<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 1, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2, a->clamped);
-    k_hist<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3, a->clamped);
-    k_bounds<NT><<<(int)T, NT, 0, s>>>(*pool, a->seq_rows, S);
-  }
-  if (a->n_seqs > 0) {
-    k_select<<<a->n_seqs, 1024, 0, s>>>(S, pool->block_size, a->evict, a->move_offsets, pool->status);
-    k_offsets<<<1, 1024, 0, s>>>(S, a->n_seqs, a->move_offsets);
+    launch_pdl(k_load<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, a->budgets, S, 1, a->clamped);
+    launch_pdl(k_hist<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2,
+               a->clamped);
+    launch_pdl(k_hist<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3,
+               a->clamped);
+    launch_pdl(k_bounds<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, a->n_seqs, pool->block_size,
+               a->evict, a->move_offsets);
   }
   KVC_CHECK_LAUNCH();
   return KVC_OK;
 }
 
+// TMA variant of k_copy_published: one lane per warp moves each 16-move half
+// chunk as bulk copies (K row and V row of every move: global -> shared ->
+// global) through a two-stage per-warp staging area, so a small CTA keeps
+// 16 KB per warp in flight with few registers and fits beside two compact16
+// CTAs from the start.
+constexpr int kBulkWarps = 4;
+__global__ void __launch_bounds__(kBulkWarps * 32) k_copy_bulk(kvc_pool p, EvictState S, MoveArgs M) {
+  extern __shared__ __align__(128) unsigned char stage_mem[];
+  __shared__ __align__(8) uint64_t bar[kBulkWarps][2];
+  __shared__ int2 sd_s[kBulkWarps][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int T = (int)M.n_heads;
+  const uint32_t row = (uint32_t)p.head_dim * 2;  // bytes of one K (or V) row
+  const uint32_t half_bytes = 16 * 2 * row;
+  unsigned char *st[2] = {stage_mem + (size_t)warp * 2 * half_bytes, stage_mem + (size_t)warp * 2 * half_bytes + half_bytes};
+  char *kc = reinterpret_cast<char *>(p.k_cache);
+  char *vc = reinterpret_cast<char *>(p.v_cache);
+  if (lane == 0) {
+    mbar_init(&bar[warp][0], 1);
+    mbar_init(&bar[warp][1], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const uint64_t pol = policy_evict_first();
+  uint32_t phase[2] = {0, 0};
+  int it = 0;                 // halves issued by this warp
+  int pend_n = 0, pend_s = 0; // the half whose loads are in flight
+  const int2 *pend_sd = nullptr;
+  unsigned long long t0 = 0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  // store the in-flight half once its loads land
+  auto drain_pending = [&]() {
+    if (lane == 0 && pend_n) {
+      mbar_wait(&bar[warp][pend_s], phase[pend_s]);
+      phase[pend_s] ^= 1;
+      for (int j = 0; j < pend_n; ++j) {
+        const int2 m = pend_sd[j];
+        const unsigned char *sk = st[pend_s] + (size_t)j * 2 * row;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(kc + (int64_t)m.y * row),
+                     "r"(smem_u32(sk)), "r"(row) : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(vc + (int64_t)m.y * row),
+                     "r"(smem_u32(sk + row)), "r"(row) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    pend_n = 0;
+  };
+  for (;;) {
+    unsigned long long d = 0;
+    if (lane == 0) {
+      const int id = atomicAdd(S.claim_next, 1);
+      for (int spin = 0;; ++spin) {
+        d = id < S.max_chunks ? ld_acquire64(S.chunks + id) : 0;
+        if (d) break;
+        if (ld_acquire(S.pub_count) == T && id >= __ldcg(S.chunk_tail)) break;
+        if ((spin & 63) == 63) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+          if (t - t0 > 2000000000ull) {
+            set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, -1, id);
+            break;
+          }
+        }
+        __nanosleep(128);
+      }
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (!d) break;
+    const int64_t h = (int64_t)(d >> 32) - 1;
+    const int k0 = (int)(d & 0xffffffffu) * 32;
+    const int nm = __ldcg(S.kv_ready + h) - 1;
+    const int cnt = nm - k0 < 32 ? nm - k0 : 32;
+    // the pairs of the previous chunk may still be read by drain_pending
+    drain_pending();
+    __syncwarp();
+    const int2 *mv = reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h) + k0;
+    if (lane < cnt) sd_s[warp][lane] = __ldcg(mv + lane);
+    __syncwarp();
+    for (int hb = 0; hb < cnt; hb += 16) {
+      const int n = cnt - hb < 16 ? cnt - hb : 16;
+      const int sidx = it & 1;
+      if (lane == 0) {
+        // the stage's previous stores (two halves back, the newest committed
+        // group: the last half's stores are issued below) must have read it
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_expect_tx(&bar[warp][sidx], (uint32_t)n * 2 * row);
+        for (int j = 0; j < n; ++j) {
+          const int2 m = sd_s[warp][hb + j];
+          unsigned char *sk = st[sidx] + (size_t)j * 2 * row;
+          bulk_g2s(sk, kc + (int64_t)m.x * row, row, &bar[warp][sidx], pol);
+          bulk_g2s(sk + row, vc + (int64_t)m.x * row, row, &bar[warp][sidx], pol);
+        }
+      }
+      drain_pending();  // the other stage: store it while this one loads
+      pend_n = n;
+      pend_s = sidx;
+      pend_sd = &sd_s[warp][hb];
+      ++it;
+    }
+    // the last half stays pending across the next claim (its pairs stay in
+    // sd_s until drain_pending at the top of the next chunk)
+  }
+  drain_pending();
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  grid_dep_wait();
+}
+
+void launch_copy_published(int n_sm, cudaStream_t s, const kvc_pool &pool, const EvictState &S, const MoveArgs &M) {
+  static const int u = getenv("KVC_COPY_U") ? atoi(getenv("KVC_COPY_U")) : 8;
+  static const int ctas = getenv("KVC_COPY_CTAS") ? atoi(getenv("KVC_COPY_CTAS")) : 0;
+  if (u == 8) launch_pdl(k_copy_published<8>, dim3((ctas ? ctas : 4) * n_sm), dim3(256), 0, s, pool, S, M);
+  else if (u == 4) launch_pdl(k_copy_published<4>, dim3((ctas ? ctas : 4) * n_sm), dim3(256), 0, s, pool, S, M);
+  else {
+    const size_t dyn = (size_t)kBulkWarps * 2 * 16 * 2 * pool.head_dim * 2;
+    static bool conf = false;
+    if (!conf) {
+      cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      conf = true;
+    }
+    launch_pdl(k_copy_bulk, dim3((ctas ? ctas : 1) * n_sm), dim3(kBulkWarps * 32), dyn, s, pool, S, M);
+  }
+}
+
 int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s, bool copy_kv = true) {
   const int64_t T = (int64_t)a->n_seqs * S.hp;
-  if (a->totals) cudaMemsetAsync(a->totals, 0, 4 * sizeof(int64_t), s);
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // long heads: k_compact16 moves the K/V rows itself, its copier warps
+  // helping other heads when the round is one wave of CTAs
+  const bool c16 = pool->block_size == 16 && !small_heads(S);
+  const bool fuse = c16 && copy_kv && pool->k_cache && pool->head_dim % 8 == 0 && !getenv("KVC_K4_UNFUSED");
   MoveArgs M{a->evict, a->evicted_kvs, a->freed, a->moves, a->move_offsets, a->move_counts, a->totals,
-             copy_kv ? nullptr : a->src_pos, S.max_slots};
+             copy_kv ? nullptr : a->src_pos, S.max_slots, fuse ? 1 : 0, T};
   const int words = (int)((S.max_slots + 31) / 32);
   const int dyn = words * 8;  // bitmap + word prefixes
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_compact16<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     configured = true;
   }
   if (dyn > 200 * 1024) return KVC_ERR_UNSUPPORTED;
+  bool totals_done = false;
   if (pool->block_size == 16) {
-    static bool conf16 = false;
-    if (!conf16) {
-      cudaFuncSetAttribute(k_compact16<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      conf16 = true;
-    }
     if (small_heads(S)) {
-      k_compact_warp<<<(unsigned)((T + kWC - 1) / kWC), kWC * 32, 0, s>>>(*pool, a->seq_rows, S, M, T);
+      launch_pdl(k_compact_warp, dim3((unsigned)((T + kWC - 1) / kWC)), dim3(kWC * 32), 0, s, *pool, a->seq_rows, S,
+                 M, T);
     } else if (getenv("KVC_K4_TRACE")) {
       // debug: per-phase time of k_compact16 averaged over the heads (synchronises)
       unsigned long long *tr = nullptr;
@@ -1924,37 +2491,42 @@ int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cu
       cudaStreamSynchronize(s);
       cudaMemcpy(h, tr, T * 64, cudaMemcpyDeviceToHost);
       double acc[7] = {0};
-      unsigned long long t0 = ~0ull, t1 = 0;
+      unsigned long long t0 = ~0ull, t1 = 0, pub_max = 0, pub_min = ~0ull;
       int n = 0;
       for (int64_t g = 0; g < T; ++g) {
         if (!h[g * 8 + 6]) continue;
         ++n;
         t0 = h[g * 8] < t0 ? h[g * 8] : t0;
-        t1 = h[g * 8 + 6] > t1 ? h[g * 8 + 6] : t1;
-        for (int k = 0; k < 6; ++k) acc[k] += (double)(h[g * 8 + k + 1] - h[g * 8 + k]) / 1e3;
+        t1 = h[g * 8 + 7] > t1 ? h[g * 8 + 7] : t1;
+        pub_max = h[g * 8 + 3] > pub_max ? h[g * 8 + 3] : pub_max;
+        pub_min = h[g * 8 + 3] < pub_min ? h[g * 8 + 3] : pub_min;
+        for (int k = 0; k < 7; ++k) acc[k] += (double)(h[g * 8 + k + 1] - h[g * 8 + k]) / 1e3;
       }
-      fprintf(stderr, "[k4 trace] heads %d span %.1f us; per head: T_h %.1f tie %.1f pairing %.1f meta %.1f free %.1f renumber %.1f us\n",
-              n, (t1 - t0) / 1e3, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+      fprintf(stderr, "[k4 trace] heads %d span %.1f us (move lists published %.1f-%.1f us); per head: T_h %.1f tie %.1f "
+              "pairing %.1f meta %.1f free %.1f renumber %.1f, then K/V copy to CTA end %.1f us\n",
+              n, (t1 - t0) / 1e3, (pub_min - t0) / 1e3, (pub_max - t0) / 1e3, acc[0] / n, acc[1] / n, acc[2] / n,
+              acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n);
       free(h);
       cudaFree(tr);
+      if (fuse) launch_copy_published(n_sm, s, *pool, S, M);
     }
-    else if (dyn <= 100 * 1024) k_compact16<512><<<(int)T, 512, dyn, s>>>(*pool, a->seq_rows, S, M);
+    else if (dyn <= 100 * 1024) launch_pdl(k_compact16<512>, dim3((unsigned)T), dim3(512), dyn, s, *pool, a->seq_rows, S, M);
     else return KVC_ERR_UNSUPPORTED;
+    // K/V moves beside the compaction, in publication order
+    if (fuse) launch_copy_published(n_sm, s, *pool, S, M);
+    totals_done = !small_heads(S) && !getenv("KVC_K4_TRACE");  // k_compact16's last CTA
   } else {
-    k_compact<<<(int)T, kThreads, dyn, s>>>(*pool, a->seq_rows, S, M);
+    launch_pdl(k_compact, dim3((unsigned)T), dim3(kThreads), dyn, s, *pool, a->seq_rows, S, M);
   }
-  if (copy_kv && pool->k_cache && T > 0) {
-    static int n_sm = 0;
-    if (!n_sm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
+  if (copy_kv && pool->k_cache && T > 0 && !fuse) {
     // short heads (few moves each): one flat grid; long heads: a CTA row per head
-    if (small_heads(S)) k_copy_kv<<<n_sm * 8, 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts, T);
-    else k_copy_kv_heads<<<dim3((unsigned)T, 8), 256, 0, s>>>(*pool, a->moves, a->move_offsets, a->move_counts);
+    if (small_heads(S))
+      launch_pdl(k_copy_kv, dim3(n_sm * 8), dim3(256), 0, s, *pool, a->moves, a->move_offsets, a->move_counts, T);
+    else
+      launch_pdl(k_copy_kv_heads, dim3((unsigned)T, 8), dim3(256), 0, s, *pool, a->moves, a->move_offsets,
+                 a->move_counts);
   }
-  if (a->totals) k_free_total<<<1, 1024, 0, s>>>(*pool, a->totals);
+  if (a->totals && !totals_done) launch_pdl(k_free_total, dim3(1), dim3(1024), 0, s, *pool, a->totals);
   KVC_CHECK_LAUNCH();
   return KVC_OK;
 }
@@ -1982,8 +2554,12 @@ int kvc_execute_moves(const kvc_pool *pool, const kvc_evict_args *a, void *strea
   cudaStream_t s = (cudaStream_t)stream;
   // keys are recomputed so the call is self-contained
   const int64_t T = (int64_t)a->n_seqs * S.hp;
-  if (small_heads(S)) k_load<256><<<(int)T, 256, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0, a->clamped);
-  else k_load<kThreads><<<(int)T, kThreads, 0, s>>>(*pool, a->seq_rows, a->budgets, S, 0, a->clamped);
+  cudaMemsetAsync(S.zero, 0, S.zero_n * sizeof(int32_t), s);
+  if (small_heads(S))
+    launch_pdl(k_load<256>, dim3((unsigned)T), dim3(256), 0, s, *pool, a->seq_rows, a->budgets, S, 0, a->clamped);
+  else
+    launch_pdl(k_load<kThreads>, dim3((unsigned)T), dim3(kThreads), 0, s, *pool, a->seq_rows, a->budgets, S, 0,
+               a->clamped);
   return run_compact(pool, a, S, s);
 }
 
@@ -2000,8 +2576,8 @@ int kvc_prefill_compress(const kvc_pool *pool, const kvc_evict_args *a, const vo
   cudaStream_t s = (cudaStream_t)stream;
   if ((rc = run_schedule(pool, a, S, s))) return rc;
   if ((rc = run_compact(pool, a, S, s, /*copy_kv=*/false))) return rc;
-  k_place_prompt_kv<<<dim3((unsigned)S.hp, 4), 256, 0, s>>>(*pool, a->seq_rows, S.hp, a->evict, a->src_pos,
-                                                             S.max_slots, (const uint4 *)k, (const uint4 *)v, L);
+  launch_pdl(k_place_prompt_kv, dim3((unsigned)S.hp, 4), dim3(256), 0, s, *pool, a->seq_rows, S.hp, a->evict,
+             a->src_pos, S.max_slots, (const uint4 *)k, (const uint4 *)v, L);
   KVC_CHECK_LAUNCH();
   return KVC_OK;
 }

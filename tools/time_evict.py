@@ -30,11 +30,13 @@ for rnd in range(4):
     k2 = e0.elapsed_time(e1)
     E = K.budget_to_blocks(L // 8, l, H, b, tables.sequence_block_count(rnd))
     e4, e5 = ev(), ev()
+    torch.cuda._sleep(4_000_000)  # hold the stream (~2 ms) so the events time device work, not host enqueue
     e4.record()
     K.compression.schedule_evictions(tables, store, {rnd: E}, manager=mgr)  # K3 alone (no state change)
     e5.record()
     torch.cuda.synchronize()
     e2, e3 = ev(), ev()
+    torch.cuda._sleep(4_000_000)
     t0 = time.perf_counter()
     plan = K.compress(cache, tables, mgr, store, {rnd: E}, sync=False, events=(e2, e3))
     t1 = time.perf_counter()
@@ -48,6 +50,7 @@ for rnd in range(4):
 for rnd in range(4, 7):
     e0, e1 = ev(), ev()
     torch.cuda.synchronize()
+    torch.cuda._sleep(4_000_000)
     K.prefill_compress_sequence(cache, tables, mgr, store, rnd, q, k, v, K.MetricConfig(),
                                 K.budget_to_blocks(L // 8, l, H, b, l * H * (L // b)), sync=False, events=(e0, e1))
     torch.cuda.synchronize()
