@@ -77,8 +77,11 @@ struct EvictState {
   int32_t *done;      // [n_seqs] heads finished in the current histogram kernel (last one finds the digit)
   int32_t *done_all;  // [1] sequences whose select finished (the last one makes the offsets global)
   int32_t *kv_ready;  // [T] K/V move list published by the head's compaction CTA: moves + 1 (0 = not yet)
-  int32_t *kv_next;   // [T] next K/V copy chunk of the head to claim
   int32_t *c16_done;  // [1] k_compact16 CTAs finished (the last one sums the free tiles)
+  // long heads: the last digit level also yields the bounds (no k_bounds pass)
+  int32_t *cum3;      // [T][1024] inclusive level-3 histogram of the keys matching T*'s top 22 bits
+  int32_t *below3;    // [T] keys whose top 22 bits are below T*'s
+  int32_t *lt1p;      // [T] keys with T*'s top 11 bits but lower top 22 bits
   // K/V copy queue: each published head appends its 32-move chunks
   int32_t *pub_count;  // [1] heads published
   int32_t *chunk_tail; // [1] chunks appended
@@ -519,6 +522,120 @@ __global__ void __launch_bounds__(NT) k_bounds(kvc_pool p, const int32_t *rows, 
   bounds_body<NT>(p, rows, S, n_seqs, bsz, evict, move_off);
 }
 
+// (5-8) long heads: the last digit level (10 bits of the keys matching T*'s
+// top 22) with the bounds folded in.  Each head CTA keeps its inclusive
+// histogram and its counts below the prefix; once the sequence's last CTA
+// has T*, the per-head counts follow from them (rows < / <= T*, and the keys
+// below T* that share its top 11 / 22 bits), so no pass re-reads the keys.
+// That CTA then takes the tie rows (select_seq); the last sequence makes the
+// move offsets global.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_hist_final(kvc_pool p, const int32_t *rows, EvictState S, const int64_t *req,
+                                                        int64_t *clamped, int n_seqs, int bsz, int32_t *evict,
+                                                        int64_t *move_off) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  __shared__ int32_t hist[kBins];
+  __shared__ int32_t below_s, lt1_s;
+  const int g = blockIdx.x;
+  const int si = g / S.hp, hi = g % S.hp;
+  const int b = p.block_size;
+  const bool active = S.E[si] > 0;
+  if (active) {
+    const int64_t hidx = (int64_t)rows[si] * S.hp + hi;
+    const int64_t n = (int64_t)p.nblocks[hidx] * b;
+    const uint32_t pre = S.prefix[si];  // T*'s top 22 bits
+    const uint32_t pre1 = pre >> 11;     // its top 11
+    const uint32_t *keys = S.keys + (int64_t)g * S.max_slots;
+    for (int i = threadIdx.x; i < kBins; i += NT) hist[i] = 0;  // (the upper half stays zero for the scan)
+    if (threadIdx.x == 0) { below_s = 0; lt1_s = 0; }
+    __syncthreads();
+    int32_t below = 0, lt1 = 0;
+    constexpr int U = 8;
+    for (int64_t base = 0; base < n; base += 4 * NT * U) {
+      uint4 k4[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);  // max_slots is a multiple of 4
+        k4[u] = pos < n ? *reinterpret_cast<const uint4 *>(keys + pos) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t pos = base + 4 * ((int64_t)u * NT + threadIdx.x);
+        const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+        uint32_t bin[4];
+        bool act[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool in = pos + e < n;
+          const uint32_t top = kv[e] >> 10;
+          below += (in && top < pre) ? 1 : 0;
+          lt1 += (in && top < pre && (kv[e] >> 21) == pre1) ? 1 : 0;
+          bin[e] = kv[e] & 1023u;
+          act[e] = in && top == pre;
+        }
+        hist_add4(hist, bin, act);
+      }
+    }
+    below = __reduce_add_sync(0xffffffffu, below);
+    lt1 = __reduce_add_sync(0xffffffffu, lt1);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&below_s, below);
+      atomicAdd(&lt1_s, lt1);
+    }
+    __syncthreads();
+    scan_hist<NT>(hist);  // inclusive
+    int32_t *row = S.cum3 + (int64_t)g * 1024;
+    for (int i = threadIdx.x; i < 1024; i += NT) row[i] = hist[i];
+    if (threadIdx.x == 0) {
+      S.below3[g] = below_s;
+      S.lt1p[g] = lt1_s;
+    }
+    add_contrib<NT>(hist, below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1024);
+  }
+  if (!last_of_sequence(S, si)) return;
+  if (active) {
+    find_digit<NT>(req, S, si, 3, 10, clamped);
+    __syncthreads();
+    const uint32_t Ts = S.prefix[si];
+    const int d3 = (int)(Ts & 1023u);
+    for (int h = threadIdx.x; h < S.hp; h += NT) {
+      const int64_t gg = (int64_t)si * S.hp + h;
+      const int32_t *row = S.cum3 + gg * 1024;
+      const int32_t c_lt = d3 > 0 ? __ldcg(row + d3 - 1) : 0;
+      const int32_t c_le = __ldcg(row + d3);
+      const int32_t bl = __ldcg(S.below3 + gg);
+      const int32_t lt = bl + c_lt, le = bl + c_le;
+      const int cap = __ldcg(S.cap + gg);
+      S.lo[gg] = lt / b < cap ? lt / b : cap;
+      S.hi[gg] = le / b < cap ? le / b : cap;
+      S.ltc[gg] = lt;
+      S.lec[gg] = le;
+      S.lt2[gg] = c_lt;
+      S.lt1[gg] = __ldcg(S.lt1p + gg) + c_lt;
+    }
+    __syncthreads();
+  } else {
+    for (int h = threadIdx.x; h < S.hp; h += NT) {
+      const int64_t gg = (int64_t)si * S.hp + h;
+      S.lo[gg] = 0;
+      S.hi[gg] = 0;
+    }
+    __syncthreads();
+  }
+  select_seq<NT>(S, si, bsz, evict, move_off, p.status);
+  __shared__ int last_all;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(S.done_all) : "memory");
+    last_all = prev == n_seqs - 1;
+    if (last_all) *S.done_all = 0;
+  }
+  __syncthreads();
+  if (last_all) offsets_all<NT>(S, n_seqs, move_off);
+}
+
 
 template <int NT>
 __device__ void bounds_counts(const kvc_pool &p, const int32_t *rows, EvictState &S, int g, int si, int hi) {
@@ -797,58 +914,6 @@ __device__ __forceinline__ int32_t group_excl_scan(int32_t v, int gtid, int GT, 
   total = tot;
   return pre + x - v;
 }
-
-constexpr int kKvChunk = 32;  // moves per claim: one per lane of the claiming warp
-
-// Copier warps of k_compact16: claim 32-move chunks of head h's move list
-// until none are left (claims are atomic, so the owner CTA's warps and
-// helpers never overlap).  Each lane holds one move's (src, dst); the warp
-// then streams the K and V rows of the chunk's moves, 16-byte units per lane,
-// U units in flight.  Sources sit in blocks this round frees: read once,
-// streamed.
-__device__ void kv_drain(const kvc_pool &p, const EvictState &S, const MoveArgs &M, int64_t h, int nm) {
-  constexpr int U = 8;
-  const int lane = threadIdx.x & 31;
-  const int vec = p.head_dim / 8, cm = 2 * vec;  // 16-byte units per move (K row, then V row)
-  uint4 *kc = reinterpret_cast<uint4 *>(p.k_cache);
-  uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
-  const int2 *mv = reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h);
-  const int nch = (nm + kKvChunk - 1) / kKvChunk;
-  for (;;) {
-    int c = 0;
-    if (lane == 0) c = atomicAdd(&S.kv_next[h], 1);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= nch) break;
-    const int k0 = c * kKvChunk;
-    const int cnt = nm - k0 < kKvChunk ? nm - k0 : kKvChunk;
-    int2 sd = make_int2(0, 0);
-    if (lane < cnt) sd = __ldcg(mv + k0 + lane);
-    const int units = cnt * cm;
-    for (int b = 0; b < units; b += 32 * U) {
-      uint4 val[U];
-      uint4 *dst[U];
-#pragma unroll
-      for (int i = 0; i < U; ++i) {
-        const int u = b + i * 32 + lane;
-        const int j = u / cm;  // move of this unit (lanes past the chunk read lane j's pair harmlessly)
-        const int src = __shfl_sync(0xffffffffu, sd.x, j & 31);
-        const int dd = __shfl_sync(0xffffffffu, sd.y, j & 31);
-        dst[i] = nullptr;
-        if (u < units) {
-          int cc = u - j * cm;
-          uint4 *base = cc >= vec ? vc : kc;
-          cc -= cc >= vec ? vec : 0;
-          val[i] = __ldcs(base + (int64_t)src * vec + cc);
-          dst[i] = base + (int64_t)dd * vec + cc;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < U; ++i)
-        if (dst[i]) *dst[i] = val[i];
-    }
-  }
-}
-
 
 // k_compact16 (whole CTA): head h's move list (nm moves) is complete; append
 // its 32-move chunks to the copy queue (the list is released before the
@@ -2263,7 +2328,7 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.lt1 = sc.take<int32_t>(T);
   S.lt2 = sc.take<int32_t>(T);
   // zero-initialised block: digit deltas, arrival counters, K/V copy claims
-  S.zero_n = (int64_t)a->n_seqs * kBins + a->n_seqs + 1 + 2 * T + 1 + 3;
+  S.zero_n = (int64_t)a->n_seqs * kBins + a->n_seqs + 1 + T + 1 + 3;
   S.max_chunks = a->moves_capacity / 32 + T + 1;
   S.zero_n += 2 * S.max_chunks + 1;  // the chunk queue (u64, 8-byte aligned below)
   S.zero = sc.take<int32_t>(S.zero_n);
@@ -2271,8 +2336,7 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
   S.done = S.zero ? S.R + (int64_t)a->n_seqs * kBins : nullptr;
   S.done_all = S.zero ? S.done + a->n_seqs : nullptr;
   S.kv_ready = S.zero ? S.done_all + 1 : nullptr;
-  S.kv_next = S.zero ? S.kv_ready + T : nullptr;
-  S.c16_done = S.zero ? S.kv_next + T : nullptr;
+  S.c16_done = S.zero ? S.kv_ready + T : nullptr;
   S.pub_count = S.zero ? S.c16_done + 1 : nullptr;
   S.chunk_tail = S.zero ? S.pub_count + 1 : nullptr;
   S.claim_next = S.zero ? S.chunk_tail + 1 : nullptr;
@@ -2280,6 +2344,10 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
                           (reinterpret_cast<uintptr_t>(S.claim_next + 1) + 7) & ~uintptr_t(7))
                     : nullptr;
   S.totals = a->totals;
+  S.cum3 = small_heads(S) ? nullptr : sc.take<int32_t>(T * 1024);
+  S.below3 = small_heads(S) ? nullptr : sc.take<int32_t>(T);
+  S.lt1p = small_heads(S) ? nullptr : sc.take<int32_t>(T);
+  if (!small_heads(S) && (!S.cum3 || !S.below3 || !S.lt1p)) return KVC_ERR_INVALID;
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
   S.seq_moves = sc.take<int64_t>(a->n_seqs);
@@ -2319,136 +2387,16 @@ int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, c
     launch_pdl(k_load<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, a->budgets, S, 1, a->clamped);
     launch_pdl(k_hist<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, 21, 10, 11, a->budgets, 2,
                a->clamped);
-    launch_pdl(k_hist<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, 10, 0, 10, a->budgets, 3,
-               a->clamped);
-    launch_pdl(k_bounds<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, a->n_seqs, pool->block_size,
-               a->evict, a->move_offsets);
+    launch_pdl(k_hist_final<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, a->budgets, a->clamped,
+               a->n_seqs, pool->block_size, a->evict, a->move_offsets);
   }
   KVC_CHECK_LAUNCH();
   return KVC_OK;
 }
 
-// TMA variant of k_copy_published: one lane per warp moves each 16-move half
-// chunk as bulk copies (K row and V row of every move: global -> shared ->
-// global) through a two-stage per-warp staging area, so a small CTA keeps
-// 16 KB per warp in flight with few registers and fits beside two compact16
-// CTAs from the start.
-constexpr int kBulkWarps = 4;
-__global__ void __launch_bounds__(kBulkWarps * 32) k_copy_bulk(kvc_pool p, EvictState S, MoveArgs M) {
-  extern __shared__ __align__(128) unsigned char stage_mem[];
-  __shared__ __align__(8) uint64_t bar[kBulkWarps][2];
-  __shared__ int2 sd_s[kBulkWarps][32];
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int T = (int)M.n_heads;
-  const uint32_t row = (uint32_t)p.head_dim * 2;  // bytes of one K (or V) row
-  const uint32_t half_bytes = 16 * 2 * row;
-  unsigned char *st[2] = {stage_mem + (size_t)warp * 2 * half_bytes, stage_mem + (size_t)warp * 2 * half_bytes + half_bytes};
-  char *kc = reinterpret_cast<char *>(p.k_cache);
-  char *vc = reinterpret_cast<char *>(p.v_cache);
-  if (lane == 0) {
-    mbar_init(&bar[warp][0], 1);
-    mbar_init(&bar[warp][1], 1);
-    fence_barrier_init();
-  }
-  __syncwarp();
-  const uint64_t pol = policy_evict_first();
-  uint32_t phase[2] = {0, 0};
-  int it = 0;                 // halves issued by this warp
-  int pend_n = 0, pend_s = 0; // the half whose loads are in flight
-  const int2 *pend_sd = nullptr;
-  unsigned long long t0 = 0;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-  // store the in-flight half once its loads land
-  auto drain_pending = [&]() {
-    if (lane == 0 && pend_n) {
-      mbar_wait(&bar[warp][pend_s], phase[pend_s]);
-      phase[pend_s] ^= 1;
-      for (int j = 0; j < pend_n; ++j) {
-        const int2 m = pend_sd[j];
-        const unsigned char *sk = st[pend_s] + (size_t)j * 2 * row;
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(kc + (int64_t)m.y * row),
-                     "r"(smem_u32(sk)), "r"(row) : "memory");
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(vc + (int64_t)m.y * row),
-                     "r"(smem_u32(sk + row)), "r"(row) : "memory");
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    pend_n = 0;
-  };
-  for (;;) {
-    unsigned long long d = 0;
-    if (lane == 0) {
-      const int id = atomicAdd(S.claim_next, 1);
-      for (int spin = 0;; ++spin) {
-        d = id < S.max_chunks ? ld_acquire64(S.chunks + id) : 0;
-        if (d) break;
-        if (ld_acquire(S.pub_count) == T && id >= __ldcg(S.chunk_tail)) break;
-        if ((spin & 63) == 63) {
-          unsigned long long t;
-          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-          if (t - t0 > 2000000000ull) {
-            set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, -1, id);
-            break;
-          }
-        }
-        __nanosleep(128);
-      }
-    }
-    d = __shfl_sync(0xffffffffu, d, 0);
-    if (!d) break;
-    const int64_t h = (int64_t)(d >> 32) - 1;
-    const int k0 = (int)(d & 0xffffffffu) * 32;
-    const int nm = __ldcg(S.kv_ready + h) - 1;
-    const int cnt = nm - k0 < 32 ? nm - k0 : 32;
-    // the pairs of the previous chunk may still be read by drain_pending
-    drain_pending();
-    __syncwarp();
-    const int2 *mv = reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h) + k0;
-    if (lane < cnt) sd_s[warp][lane] = __ldcg(mv + lane);
-    __syncwarp();
-    for (int hb = 0; hb < cnt; hb += 16) {
-      const int n = cnt - hb < 16 ? cnt - hb : 16;
-      const int sidx = it & 1;
-      if (lane == 0) {
-        // the stage's previous stores (two halves back, the newest committed
-        // group: the last half's stores are issued below) must have read it
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_expect_tx(&bar[warp][sidx], (uint32_t)n * 2 * row);
-        for (int j = 0; j < n; ++j) {
-          const int2 m = sd_s[warp][hb + j];
-          unsigned char *sk = st[sidx] + (size_t)j * 2 * row;
-          bulk_g2s(sk, kc + (int64_t)m.x * row, row, &bar[warp][sidx], pol);
-          bulk_g2s(sk + row, vc + (int64_t)m.x * row, row, &bar[warp][sidx], pol);
-        }
-      }
-      drain_pending();  // the other stage: store it while this one loads
-      pend_n = n;
-      pend_s = sidx;
-      pend_sd = &sd_s[warp][hb];
-      ++it;
-    }
-    // the last half stays pending across the next claim (its pairs stay in
-    // sd_s until drain_pending at the top of the next chunk)
-  }
-  drain_pending();
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  grid_dep_wait();
-}
-
 void launch_copy_published(int n_sm, cudaStream_t s, const kvc_pool &pool, const EvictState &S, const MoveArgs &M) {
-  static const int u = getenv("KVC_COPY_U") ? atoi(getenv("KVC_COPY_U")) : 8;
-  static const int ctas = getenv("KVC_COPY_CTAS") ? atoi(getenv("KVC_COPY_CTAS")) : 0;
-  if (u == 8) launch_pdl(k_copy_published<8>, dim3((ctas ? ctas : 4) * n_sm), dim3(256), 0, s, pool, S, M);
-  else if (u == 4) launch_pdl(k_copy_published<4>, dim3((ctas ? ctas : 4) * n_sm), dim3(256), 0, s, pool, S, M);
-  else {
-    const size_t dyn = (size_t)kBulkWarps * 2 * 16 * 2 * pool.head_dim * 2;
-    static bool conf = false;
-    if (!conf) {
-      cudaFuncSetAttribute(k_copy_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      conf = true;
-    }
-    launch_pdl(k_copy_bulk, dim3((ctas ? ctas : 1) * n_sm), dim3(kBulkWarps * 32), dyn, s, pool, S, M);
-  }
+  // 4 CTAs per SM: they take the SMs as k_compact16's CTAs leave them
+  launch_pdl(k_copy_published<8>, dim3(4 * n_sm), dim3(256), 0, s, pool, S, M);
 }
 
 int run_compact(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, cudaStream_t s, bool copy_kv = true) {
