@@ -212,7 +212,7 @@ def _scratch_bytes(plan: EvictionPlan, hp: int) -> int:
     # + the K/V copy queue (one u64 per 32 moves of capacity, + one per head)
     cap = plan.moves.shape[0] if plan.moves is not None else 0
     return (T * ((plan.max_slots + 3) // 4 * 4) * 4 + T * 36 + n * (2048 * 4 + 44) + T * 2 * 256 * 8
-            + (cap // 32 + T + 2) * 8 + (T * (1024 + 2) * 4 if plan.max_slots > 8192 else 0) + (1 << 16))
+            + (cap // 32 + T + 2) * 8 + (T * (2 * 2048 + 1024 + 2) * 4 if plan.max_slots > 8192 else 0) + (1 << 16))
 
 
 def schedule_evictions(tables: BlockTables, store: MetricsStore, budgets: Mapping[int, int],

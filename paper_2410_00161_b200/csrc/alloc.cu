@@ -340,7 +340,7 @@ int64_t kvc_scratch_bytes(const kvc_pool *pool, int64_t max_heads, int64_t max_s
   // K3/K4: u32 keys (rows padded to 4), 9 per-head ints, the short-head
   // candidate lists (2 x 256 u64), per-sequence digit deltas (n_seqs <= heads)
   // and the K/V copy queue (a u64 per 32 moves; moves <= slots)
-  int64_t evict = max_slots * 4 + max_slots / 2 + max_heads * (12 + 36 + 4096 + 2048 * 4 + 44 + 8 + 4104) + 65536;
+  int64_t evict = max_slots * 4 + max_slots / 2 + max_heads * (12 + 36 + 4096 + 2048 * 4 + 44 + 8 + 4104 + 16384) + 65536;
   int64_t m = alloc > decode ? alloc : decode;
   m = m > evict ? m : evict;
   return m + (1 << 20);

@@ -79,6 +79,8 @@ struct EvictState {
   int32_t *kv_ready;  // [T] K/V move list published by the head's compaction CTA: moves + 1 (0 = not yet)
   int32_t *c16_done;  // [1] k_compact16 CTAs finished (the last one sums the free tiles)
   // long heads: the last digit level also yields the bounds (no k_bounds pass)
+  int32_t *cum1;      // [T][2048] inclusive level-1 histogram (top 11 bits) of all keys
+  int32_t *cum2;      // [T][2048] inclusive level-2 histogram of the keys matching T*'s top 11 bits
   int32_t *cum3;      // [T][1024] inclusive level-3 histogram of the keys matching T*'s top 22 bits
   int32_t *below3;    // [T] keys whose top 22 bits are below T*'s
   int32_t *lt1p;      // [T] keys with T*'s top 11 bits but lower top 22 bits
@@ -378,6 +380,10 @@ __device__ bool load_body(const kvc_pool &p, const int32_t *rows, const int64_t 
   if (!with_hist) return false;
   if (req[si] > 0) {
     scan_hist<NT>(hist);
+    if (S.cum1) {  // long heads: kept for k_compact16's threshold select
+      int32_t *row = S.cum1 + (int64_t)g * kBins;
+      for (int i = threadIdx.x; i < kBins; i += NT) row[i] = hist[i];
+    }
     add_contrib<NT>(hist, 0, cap, b, S.R + (int64_t)si * kBins, kBins);
   }
   if (!last_of_sequence(S, si)) return false;
@@ -465,6 +471,10 @@ __device__ bool hist_body(const kvc_pool &p, const int32_t *rows, EvictState &S,
   if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)&below_s, (unsigned long long)below);
   __syncthreads();
   scan_hist<NT>(hist);
+  if (S.cum2 && level == 2) {  // long heads: kept for k_compact16's threshold select
+    int32_t *row = S.cum2 + (int64_t)g * kBins;
+    for (int i = threadIdx.x; i < kBins; i += NT) row[i] = hist[i];
+  }
   add_contrib<NT>(hist, (int32_t)below_s, S.cap[g], b, S.R + (int64_t)si * kBins, 1 << bits);
   if (!last_of_sequence(S, si)) return false;
   find_digit<NT>(req, S, si, level, bits, clamped);
@@ -1356,12 +1366,53 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
     } else if (S.lt1[g] > from_top) {
       lv0 = 1; pre0 = Tstar >> 21; rank0 = S.lt1[g] - 1 - from_top;
     }
-    T = select16<NT>(hist, n, rank0, [&](int64_t pos, uint32_t *v, bool *ok) {
-      const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
-      v[0] = k4.x; v[1] = k4.y; v[2] = k4.z; v[3] = k4.w;
+    if (S.cum3) {
+      // Long heads: the histograms K3 kept give the threshold's digits down
+      // to the first level that is not T*'s: level 1 from all keys' top-11
+      // histogram, level 2 from that of T*'s 11-bit bucket, level 3 from that
+      // of its 22-bit bucket (a bucket's keys below T* are its smallest, so
+      // ranks inside it are ranks among the keys below T*).  One or two key
+      // passes fewer, none when the threshold shares T*'s top 22 bits.
+      const int32_t *rows3[3] = {S.cum1 + (int64_t)g * kBins, S.cum2 + (int64_t)g * kBins,
+                                 S.cum3 + (int64_t)g * 1024};
+      const int nbins[3] = {kBins, kBins, 1024};
+      const int bitsv[3] = {11, 11, 10};
+      __shared__ uint32_t d_s;
+      __shared__ int64_t r_s, c_s;
+      const int lv = lv0;
+      const int32_t *row = rows3[lv];
+      for (int d = threadIdx.x; d < nbins[lv]; d += NT) {
+        const int32_t lo_c = d > 0 ? __ldcg(row + d - 1) : 0, hi_c = __ldcg(row + d);
+        if (lo_c <= rank0 && rank0 < hi_c) {
+          d_s = (uint32_t)d;
+          r_s = rank0 - lo_c;
+          c_s = hi_c - lo_c;
+        }
+      }
+      __syncthreads();
+      const uint32_t pre1 = (pre0 << bitsv[lv]) | d_s;
+      const int64_t rank1 = r_s, cnt1 = c_s;
+      __syncthreads();
+      if (lv == 2) {
+        T = pre1;
+        tie_rank = rank1;
+        tie_cnt = cnt1;
+      } else {
+        T = select16<NT>(hist, n, rank1, [&](int64_t pos, uint32_t *v, bool *ok) {
+          const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
+          v[0] = k4.x; v[1] = k4.y; v[2] = k4.z; v[3] = k4.w;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ok[i] = pos + i < n && v[i] < Tstar;
-    }, &tie_rank, &tie_cnt, lv0, pre0);
+          for (int i = 0; i < 4; ++i) ok[i] = pos + i < n && v[i] < Tstar;
+        }, &tie_rank, &tie_cnt, lv + 1, pre1);
+      }
+    } else {
+      T = select16<NT>(hist, n, rank0, [&](int64_t pos, uint32_t *v, bool *ok) {
+        const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + pos);
+        v[0] = k4.x; v[1] = k4.y; v[2] = k4.z; v[3] = k4.w;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ok[i] = pos + i < n && v[i] < Tstar;
+      }, &tie_rank, &tie_cnt, lv0, pre0);
+    }
   }
   if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 1] = t_; }
   // ---- tie cut: ties at T ordered by (occupied, logical, position) ----
@@ -1568,34 +1619,37 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
     group_sync(bar, GT);
     if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 4] = t_; }
     // ---- free the trailing e blocks and reset their slots ----
-    for (int t = gtid; t < e; t += GT) {
-      const int j = rb + t;
-      const int32_t blk = tab[j];
-      const int64_t f0 = (int64_t)blk * 16;
-      float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
-      int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
+    // four table entries per thread in flight; free-tile counts with one
+    // atomic per (warp, tile) (a head's blocks sit in a few tiles, so
+    // per-block atomics would serialise)
+    for (int base = 0; base < e; base += 4 * GT) {
+      int32_t blk[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        lp[q] = make_int4(-1, -1, -1, -1);
+      for (int u = 0; u < 4; ++u) {
+        const int t = base + u * GT + gtid;
+        blk[u] = t < e ? tab[rb + t] : -1;
       }
-      *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
-      p.free_flag[blk] = 1;
-      if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk;
-    }
-    {
-      // free-tile counts: one atomic per (warp, tile) instead of per block
-      // (a head's blocks sit in a few tiles, so per-block atomics serialise)
-      for (int base = 0; base < e; base += GT) {
-        const int t = base + gtid;
-        const bool act = t < e;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = base + u * GT + gtid;
+        const bool act = blk[u] >= 0;
         const unsigned am = __ballot_sync(0xffffffffu, act);
-        if (act) {
-          const int tile = tab[rb + t] / KVC_FREE_TILE;
-          const unsigned peers = __match_any_sync(am, tile);
-          if ((gtid & 31) == __ffs(peers) - 1) atomicAdd(&p.free_tile[tile], __popc(peers));
+        if (!act) continue;
+        const int64_t f0 = (int64_t)blk[u] * 16;
+        float4 *mp = reinterpret_cast<float4 *>(p.metric + f0);
+        int4 *lp = reinterpret_cast<int4 *>(p.logical + f0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          mp[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          lp[q] = make_int4(-1, -1, -1, -1);
         }
+        *reinterpret_cast<uint4 *>(p.protected_ + f0) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4 *>(p.fresh + f0) = make_uint4(0, 0, 0, 0);
+        p.free_flag[blk[u]] = 1;
+        if (M.freed) M.freed[(int64_t)g * p.max_blocks + t] = blk[u];
+        const int tile = blk[u] / KVC_FREE_TILE;
+        const unsigned peers = __match_any_sync(am, tile);
+        if ((gtid & 31) == __ffs(peers) - 1) atomicAdd(&p.free_tile[tile], __popc(peers));
       }
     }
     if (S.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); S.trace[g * 8 + 5] = t_; }
@@ -2344,10 +2398,12 @@ int setup_state(const kvc_pool *pool, const kvc_evict_args *a, Scratch &sc, Evic
                           (reinterpret_cast<uintptr_t>(S.claim_next + 1) + 7) & ~uintptr_t(7))
                     : nullptr;
   S.totals = a->totals;
+  S.cum1 = small_heads(S) ? nullptr : sc.take<int32_t>(T * kBins);
+  S.cum2 = small_heads(S) ? nullptr : sc.take<int32_t>(T * kBins);
   S.cum3 = small_heads(S) ? nullptr : sc.take<int32_t>(T * 1024);
   S.below3 = small_heads(S) ? nullptr : sc.take<int32_t>(T);
   S.lt1p = small_heads(S) ? nullptr : sc.take<int32_t>(T);
-  if (!small_heads(S) && (!S.cum3 || !S.below3 || !S.lt1p)) return KVC_ERR_INVALID;
+  if (!small_heads(S) && (!S.cum1 || !S.cum2 || !S.cum3 || !S.below3 || !S.lt1p)) return KVC_ERR_INVALID;
   S.prefix = sc.take<uint32_t>(a->n_seqs);
   S.E = sc.take<int64_t>(a->n_seqs);
   S.seq_moves = sc.take<int64_t>(a->n_seqs);

@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_compress.py tests/test_gpu_prefill_compress.py tests/test_gpu_engine.py tests/test_gpu_baseline_shapes.py -x -q -p no:cacheprovider 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_compress.py tests/test_gpu_prefill_compress.py -x -q -p no:cacheprovider 2>&1 | tail -1
 KVC_K4_TRACE=1 timeout 300 python tools/time_evict.py 2>&1 | grep "k4 trace" | sed -n 3,4p
 timeout 300 python tools/time_evict.py | python -c "import json,sys; r=json.load(sys.stdin); print('k34', [round(x['k34_ms'],4) for x in r if 'k34_ms' in x], 'k3', [round(x['k3_ms'],4) for x in r if 'k3_ms' in x], 'fused', [round(x['fused_prefill_compress_ms'],4) for x in r if 'fused_prefill_compress_ms' in x])"
