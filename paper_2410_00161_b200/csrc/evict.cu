@@ -964,6 +964,48 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 // waiting for a chunk entry cannot deadlock; a bounded wait still turns a
 // missing publication into a status error instead of a hang.  The final
 // griddepcontrol.wait makes this grid's completion imply compact16's.
+// Lane 0: the queue entry `id` once it is written (0 when the queue is
+// exhausted, or after a 2 s wait: a head never published).
+__device__ __forceinline__ unsigned long long wait_chunk(const EvictState &S, const kvc_pool &p, int id, int T,
+                                                         unsigned long long t0) {
+  for (int spin = 0;; ++spin) {
+    const unsigned long long d = id < S.max_chunks ? ld_acquire64(S.chunks + id) : 0;
+    if (d) return d;
+    if (ld_acquire(S.pub_count) == T && id >= __ldcg(S.chunk_tail)) return 0;  // all published, no more work
+    if ((spin & 63) == 63) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > 2000000000ull) {
+        set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, -1, id);
+        return 0;
+      }
+    }
+    __nanosleep(128);
+  }
+}
+
+// A chunk's moves: lane j holds move j's (src, dst); returns the move count.
+__device__ __forceinline__ int chunk_pairs(const EvictState &S, const MoveArgs &M, unsigned long long d, int lane,
+                                           int2 &sd) {
+  const int64_t h = (int64_t)(d >> 32) - 1;
+  const int k0 = (int)(d & 0xffffffffu) * 32;
+  const int nm = __ldcg(S.kv_ready + h) - 1;  // released before the chunk entry
+  const int cnt = nm - k0 < 32 ? nm - k0 : 32;
+  sd = make_int2(0, 0);
+  if (lane < cnt) sd = __ldcg(reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h) + k0 + lane);
+  return cnt;
+}
+
+// K/V rows of every move of the round, running beside k_compact16 (launched
+// programmatically: its CTAs take the SMs compact16's CTAs leave).  A warp
+// claims queue chunks (32 moves, one (src, dst) per lane); the next chunk is
+// claimed when the current one starts and its pairs are fetched halfway
+// through it, so queue latency hides under the copy.  All compact16 CTAs are
+// resident by the time this grid launches (they trigger first) and every one
+// of them publishes (0 moves when it evicts nothing), so waiting for a chunk
+// entry cannot deadlock; a bounded wait still turns a missing publication
+// into a status error instead of a hang.  The final griddepcontrol.wait makes
+// this grid's completion imply compact16's.
 template <int U>
 __global__ void __launch_bounds__(256) k_copy_published(kvc_pool p, EvictState S, MoveArgs M) {
   const int lane = threadIdx.x & 31;
@@ -973,35 +1015,19 @@ __global__ void __launch_bounds__(256) k_copy_published(kvc_pool p, EvictState S
   uint4 *vc = reinterpret_cast<uint4 *>(p.v_cache);
   unsigned long long t0 = 0;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-  for (;;) {
-    unsigned long long d = 0;
-    if (lane == 0) {
-      const int id = atomicAdd(S.claim_next, 1);
-      for (int spin = 0;; ++spin) {
-        d = id < S.max_chunks ? ld_acquire64(S.chunks + id) : 0;
-        if (d) break;
-        if (ld_acquire(S.pub_count) == T && id >= __ldcg(S.chunk_tail)) break;  // all published, no more work
-        if ((spin & 63) == 63) {
-          unsigned long long t;
-          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-          if (t - t0 > 2000000000ull) {  // 2 s: a head never published
-            set_status(p.status, KVC_DEV_SCHEDULE_CORRUPTION, -1, id);
-            break;
-          }
-        }
-        __nanosleep(128);
-      }
-    }
-    d = __shfl_sync(0xffffffffu, d, 0);
-    if (!d) break;
-    const int64_t h = (int64_t)(d >> 32) - 1;
-    const int k0 = (int)(d & 0xffffffffu) * 32;
-    const int nm = __ldcg(S.kv_ready + h) - 1;  // released before the chunk entry
-    const int cnt = nm - k0 < 32 ? nm - k0 : 32;
-    const int2 *mv = reinterpret_cast<const int2 *>(M.moves) + __ldcg(M.move_off + h) + k0;
-    int2 sd = make_int2(0, 0);
-    if (lane < cnt) sd = __ldcg(mv + lane);
+  unsigned long long d = 0;
+  if (lane == 0) d = wait_chunk(S, p, atomicAdd(S.claim_next, 1), T, t0);
+  d = __shfl_sync(0xffffffffu, d, 0);
+  int2 sd;
+  int cnt = d ? chunk_pairs(S, M, d, lane, sd) : 0;
+  while (d) {
+    int id_next = 0;
+    if (lane == 0) id_next = atomicAdd(S.claim_next, 1);
+    unsigned long long d_next = 0;
+    int2 sd_next = make_int2(0, 0);
+    int cnt_next = 0;
     const int units = cnt * cm;
+    const int half = (units / (32 * U) / 2) * 32 * U;  // the round after which the next chunk is fetched
     for (int b = 0; b < units; b += 32 * U) {
       uint4 val[U];
       uint4 *dst[U];
@@ -1020,10 +1046,18 @@ __global__ void __launch_bounds__(256) k_copy_published(kvc_pool p, EvictState S
           dst[i] = base + (int64_t)dd * vec + c;
         }
       }
+      if (b == half) {  // the next chunk's entry and pairs, while these loads are in flight
+        if (lane == 0) d_next = wait_chunk(S, p, id_next, T, t0);
+        d_next = __shfl_sync(0xffffffffu, d_next, 0);
+        if (d_next) cnt_next = chunk_pairs(S, M, d_next, lane, sd_next);
+      }
 #pragma unroll
       for (int i = 0; i < U; ++i)
         if (dst[i]) *dst[i] = val[i];
     }
+    d = d_next;
+    sd = sd_next;
+    cnt = cnt_next;
   }
   grid_dep_wait();
 }
