@@ -7,7 +7,7 @@ libkvc.so (hand-written CUDA, C ABI in include/kvc.h); there is no CPU
 fallback.
 """
 
-from .attention import AttentionConfig, gqa_attention, paged_attention, paged_decode
+from .attention import AttentionConfig, dense_attention, gqa_attention, paged_attention, paged_decode
 from .block_manager import BlockManager, blocks_needed_prefill
 from .budget import budget_to_blocks, per_sequence_budget
 from .cache import (
@@ -26,7 +26,8 @@ from .compression import (
     schedule_evictions,
 )
 from .metrics import MetricConfig, MetricsStore, accumulate_decode, full_metrics, prompt_metrics, window_metrics
-from .engine import POLICY_PRESETS, CompressionPolicy, Engine, StepRecord, select_compression_batch
+from .engine import (POLICY_PRESETS, CompressionPolicy, Engine, SequenceState, StepRecord, preempt_select,
+                     select_compression_batch)
 from .graph import DecodeStepGraph
 from .prefill import full_metrics_qk, prefill_compress_sequence, prefill_sequence, window_metrics_qk
 from .sharding import ShardedEngine, gather_counts, gather_round_counts, owner_of, shard_sequences
@@ -35,6 +36,10 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AttentionConfig",
+    "dense_attention",
+    "gqa_attention",
+    "preempt_select",
+    "SequenceState",
     "BlockManager",
     "BlockTables",
     "CompressionSchedule",
@@ -68,7 +73,6 @@ __all__ = [
     "window_metrics_qk",
     "full_metrics_qk",
     "prompt_metrics",
-    "gqa_attention",
     "ShardedEngine",
     "gather_counts",
     "gather_round_counts",

@@ -130,6 +130,13 @@ def paged_attention(query, cache: UnifiedKVCache, tables: BlockTables, seq_id: i
     return out[0], [rows[0, h, :, : ctx[h]] for h in range(cfg.num_kv_heads)]
 
 
+def dense_attention(q, k, v):
+    """Causal multi-head attention over (H, L, d) inputs (attention.py:46-59):
+    gqa_attention with one query head per KV head.  Returns (out, attn)."""
+    n, d = q.shape[0], q.shape[-1]
+    return gqa_attention(q, k, v, AttentionConfig(n, n, d, 1))
+
+
 def gqa_attention(q, k, v, cfg: AttentionConfig):
     """Dense causal grouped-query attention (attention.py:62-89): query head h
     reads KV head h // group_size.  q (n_q, L, d), k/v (n_k, L, d).  Returns

@@ -24,22 +24,32 @@ def main():
         shutil.copytree(SRC, DST)
     if "--copy-only" in sys.argv:
         return
+    xml = os.path.join(ROOT, "gpurun_out", "refsuite.xml")
+    if "--parse-only" not in sys.argv:
+        run(xml)
+    summarize(xml)
+
+
+def run(xml):
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tools", "refsuite"), ROOT, DST])
-    xml = os.path.join(ROOT, "gpurun_out", "refsuite.xml")
     os.makedirs(os.path.dirname(xml), exist_ok=True)
     subprocess.run([sys.executable, "-m", "pytest", DST, "-q", "-p", "no:cacheprovider", "--junitxml", xml,
+                    "--continue-on-collection-errors",
                     "-o", "addopts="], env=env, cwd=DST)
+
+
+def summarize(xml):
     res = {}
     for case in ET.parse(xml).getroot().iter("testcase"):
-        f = case.get("classname", "").split(".")[0] or case.get("file", "?")
+        f = case.get("classname", "").split(".")[0] or case.get("name", "?")
         r = res.setdefault(f, {"passed": 0, "failed": 0, "error": 0, "skipped": 0, "first_failures": []})
         kids = [c.tag for c in case]
         if "failure" in kids or "error" in kids:
             key = "failed" if "failure" in kids else "error"
             r[key] += 1
             if len(r["first_failures"]) < 4:
-                el = case.find(key)
+                el = case.find("failure" if key == "failed" else "error")
                 r["first_failures"].append(f"{case.get('name')}: {(el.get('message') or '')[:160]}")
         elif "skipped" in kids:
             r["skipped"] += 1

@@ -51,8 +51,17 @@ def main():
     K.compress(rig.cache, rig.tables, rig.manager, rig.store, E)
     ctx.raise_status()
 
-    # fused prefill + compress and the unfused prompt path, one small sequence
-    L, H2, r2, d2, l2 = 700, 2, 4, 128, 2
+    # fused prefill + compress and the unfused prompt path: a short prompt
+    # (warp-per-head compaction) and a long one (> 8192 slots per head: K3's
+    # last-level bounds, k_compact16 and the concurrent K/V copy kernel)
+    for L in (700, 9000):
+        prompt_rounds(K, DevRig, ctx, L)
+    print("sanitize workload done")
+
+
+def prompt_rounds(K, DevRig, ctx, L):
+    b = 16
+    H2, r2, d2, l2 = 2, 4, 128, 2
     qf = torch.randn((l2, H2 * r2, 8, d2), device="cuda").to(torch.bfloat16)
     kf = torch.randn((l2, H2, L, d2), device="cuda").to(torch.bfloat16)
     vf = torch.randn((l2, H2, L, d2), device="cuda").to(torch.bfloat16)
@@ -61,13 +70,12 @@ def main():
         rig2 = DevRig(nb, b, d2, l2, H2, max_seqs=2, max_blocks=L // b + 4)
         if fused:
             K.prefill_compress_sequence(rig2.cache, rig2.tables, rig2.manager, rig2.store, 0, qf, kf, vf,
-                                        K.MetricConfig(), 40)
+                                        K.MetricConfig(), L // 16)
         else:
             K.prefill_sequence(rig2.cache, rig2.tables, rig2.manager, rig2.store, 0, qf, kf, vf, K.MetricConfig())
-            K.compress(rig2.cache, rig2.tables, rig2.manager, rig2.store, {0: 40})
+            K.compress(rig2.cache, rig2.tables, rig2.manager, rig2.store, {0: L // 16})
         torch.cuda.synchronize()
         ctx.raise_status()
-    print("sanitize workload done")
 
 
 if __name__ == "__main__":
