@@ -906,9 +906,11 @@ int launch(Params &P, cudaStream_t s) {
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
     const int pairs_b = P.batch * P.p.num_kv_heads;
     // small batches: several CTAs per (sequence, head) share the merge and
-    // the metric pass (measured best: 8 / 4-8 / 2 / 1 CTAs at 8 / 64 / 256 /
-    // >= 512 pairs; each CTA folds the head statistics itself)
-    int ms = 512 / (pairs_b > 0 ? pairs_b : 1);
+    // the metric pass (round 2, inside the CUDA-graph step: 8 / 4 / 1 CTAs
+    // best at 8 / 64 / 256 pairs (B = 1 / 8 / 32 at 8 heads): B = 8 1.24 ->
+    // 1.06 ms and B = 32 3.26 -> 3.08 ms per step against the round-1 rule
+    // 512 / pairs; each CTA folds the head statistics itself)
+    int ms = 256 / (pairs_b > 0 ? pairs_b : 1);
     ms = ms < 1 ? 1 : ms > 8 ? 8 : ms;
     static const int ms_forced = getenv("KVC_K1_MSPLIT") ? atoi(getenv("KVC_K1_MSPLIT")) : 0;  // experiments
     if (ms_forced > 0) ms = ms_forced;
@@ -925,7 +927,8 @@ int launch(Params &P, cudaStream_t s) {
     cudaStream_t ms = reinterpret_cast<cudaStream_t>(P.metric_stream);
     cudaEventRecord(ev[dev], s);
     cudaStreamWaitEvent(ms, ev[dev], 0);
-    int msplit = 512 / (pairs > 0 ? pairs : 1);
+    static const int mm_div = getenv("KVC_K1_METRIC_DIV") ? atoi(getenv("KVC_K1_METRIC_DIV")) : 512;  // experiments
+    int msplit = mm_div / (pairs > 0 ? pairs : 1);
     msplit = msplit < 1 ? 1 : msplit > 8 ? 8 : msplit;
     k_decode_metric<D><<<dim3(pairs, msplit), 256, 0, ms>>>(P);
   }
