@@ -927,7 +927,7 @@ int launch(Params &P, cudaStream_t s) {
     cudaStream_t ms = reinterpret_cast<cudaStream_t>(P.metric_stream);
     cudaEventRecord(ev[dev], s);
     cudaStreamWaitEvent(ms, ev[dev], 0);
-    static const int mm_div = getenv("KVC_K1_METRIC_DIV") ? atoi(getenv("KVC_K1_METRIC_DIV")) : 512;  // experiments
+    static const int mm_div = getenv("KVC_K1_METRIC_DIV") ? atoi(getenv("KVC_K1_METRIC_DIV")) : 256;  // experiments
     int msplit = mm_div / (pairs > 0 ? pairs : 1);
     msplit = msplit < 1 ? 1 : msplit > 8 ? 8 : msplit;
     k_decode_metric<D><<<dim3(pairs, msplit), 256, 0, ms>>>(P);
