@@ -157,14 +157,17 @@ def peaks():
 
 
 def k1_traffic():
-    """DRAM bytes of one K1 layer launch (stream + finish kernels) from the
-    committed ncu --set full capture (profiles/r1_ncu.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu.json")) as fh:
-            d = json.load(fh)
-        return float(sum(r["dram_read_B"] + r["dram_write_B"] for r in d["k1"]))
-    except Exception:
-        return None
+    """DRAM bytes of one K1 layer launch (stream + finish + metric kernels)
+    from the newest committed ncu --set full capture (profiles/r*_ncu.json)
+    and that file's name, or (None, None)."""
+    for name in ("r2_ncu.json", "r1_ncu.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                d = json.load(fh)
+            return float(sum(r["dram_read_B"] + r["dram_write_B"] for r in d["k1"])), name
+        except Exception:
+            continue
+    return None, None
 
 
 def build(args, dev, rank):
@@ -872,9 +875,9 @@ def main():
                      "kernel": "K1 per layer: k_decode_stream + k_decode_finish (+ k_decode_metric, graph side branch)",
                      "achieved": dec["k1_gbs"] if world == 1 else k1_gbs, "peak": peak, "unit": "GB/s",
                      "frac": (dec["k1_gbs"] if world == 1 else k1_gbs) / peak,
-                     "peak_source": peak_kind, "traffic": k1_traffic(),
-                     "traffic_source": "profiles/r1_ncu.json: dram bytes of one K1 layer launch from a committed "
-                                       "ncu --set full capture (not measured in this run)",
+                     "peak_source": peak_kind, "traffic": k1_traffic()[0],
+                     "traffic_source": f"profiles/{k1_traffic()[1]}: dram bytes of one K1 layer launch from a "
+                                       "committed ncu --set full capture (not measured in this run)",
                      "bytes_per_launch": dec["k1_bytes_mean"], "launch_ms": dec["k1_ms_mean"],
                      "timing": dec["k1_timing"] + ("; per GPU, slowest rank" if world > 1 else "")},
         "eviction_step": evict,

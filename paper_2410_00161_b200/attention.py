@@ -4,7 +4,9 @@ Drop-in for pagedkv.attention.paged_attention (attention.py:92-127) plus the
 batched, fused engine path ``paged_decode``: one launch per layer appends the
 step's K/V, attends every (sequence, KV head) of the batch and folds the
 attention mass into the eviction metrics (engine.py:426-444,
-metrics.py:189-211).  Both run the same sm_100a kernel (csrc/decode.cu).
+metrics.py:189-211).  Both run the same sm_100a kernels: csrc/decode_mma.cu
+(block size 16, head_dim 64/128/256, group <= 8: TMA ring + mma.sync, split-KV)
+and csrc/decode.cu for the other shapes.
 """
 
 from __future__ import annotations

@@ -46,8 +46,15 @@ class DecodeStepGraph:
 
     def __init__(self, cache: UnifiedKVCache, tables: BlockTables, manager: BlockManager, store: MetricsStore,
                  seq_ids, cfg: AttentionConfig, metric_mode: int = 2, fresh: bool = True, headroom: int = 256,
-                 buffers: dict | None = None, metric_overlap: bool = True, host_io: list | None = None):
+                 buffers: dict | None = None, metric_overlap: bool = True, host_io: list | None = None,
+                 allocate: bool = True, clear_fresh: bool = True):
+        """allocate / clear_fresh: include the K0 decode allocation and the
+        fresh-flag clear in the step (a caller that allocates itself - the
+        Engine, which must see PreemptionNeeded before decoding - turns
+        them off and replays the layers only)."""
         self.cache, self.tables, self.manager, self.store = cache, tables, manager, store
+        self.allocate = allocate
+        self.clear_fresh = clear_fresh
         self.seq_ids = list(seq_ids)
         self.cfg = cfg
         self.metric_mode = metric_mode
@@ -171,8 +178,9 @@ class DecodeStepGraph:
                         ev = torch.cuda.Event()
                         ev.record(self.io_in)
                         ev_in.append(ev)
-            _lib.check(lib.kvc_alloc_decode(ctypes.byref(p), self.rows_sorted_t.data_ptr(), B, self.counts.data_ptr(),
-                                            stream), "alloc_decode")
+            if self.allocate:
+                _lib.check(lib.kvc_alloc_decode(ctypes.byref(p), self.rows_sorted_t.data_ptr(), B,
+                                                self.counts.data_ptr(), stream), "alloc_decode")
             done = []
             # only the first layer of each doubling group (layers 0 | 1 | 2-3 |
             # 4-7 | ...) waits for the uploads of its group: an extra graph
@@ -212,7 +220,8 @@ class DecodeStepGraph:
                 ev = torch.cuda.Event()
                 ev.record(self.io_out)
                 s.wait_event(ev)
-            _lib.check(lib.kvc_clear_fresh(ctypes.byref(p), self.rows_t.data_ptr(), B, stream), "clear_fresh")
+            if self.clear_fresh:
+                _lib.check(lib.kvc_clear_fresh(ctypes.byref(p), self.rows_t.data_ptr(), B, stream), "clear_fresh")
 
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(dev)
@@ -261,9 +270,11 @@ class DecodeStepGraph:
     def _eager_step(self) -> None:
         """The same step through paged_decode (kernel attributes, tensor maps)."""
         from .attention import paged_decode
-        self.manager.allocate_decode_step(self.seq_ids, sync=False)
+        if self.allocate:
+            self.manager.allocate_decode_step(self.seq_ids, sync=False)
         for m in range(self.tables.num_layers):
             paged_decode(self.q[m], self.cache, self.tables, None, m, self.cfg, store=self.store,
                          metric_mode=self.metric_mode, k_new=self.k_new[m], v_new=self.v_new[m], fresh=self.fresh,
                          out=self.out[m], rows_tensor=self.rows_t, host_rows=self.rows, early_pull=m > 0)
-        self.store.clear_fresh(self.tables, self.seq_ids)
+        if self.clear_fresh:
+            self.store.clear_fresh(self.tables, self.seq_ids)

@@ -11,7 +11,7 @@ ncu --set full --clock-control none --import-source on -k regex:"k_decode_stream
 K2_LAYERS=32 ncu --set full --clock-control none --import-source on -k regex:k_window_persist -s 1 -c 1 \
     -o $O/prof_k2 python tools/time_k2.py > $O/p2.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_load|k_hist|k_bounds|k_select|k_offsets|k_compact16|k_copy_kv_heads|k_place_prompt_kv" -s 20 -c 20 \
+    -k regex:"k_load|k_hist|k_compact16|k_copy_published|k_place_prompt_kv" -s 16 -c 16 \
     -o $O/prof_k34 python tools/time_evict.py > $O/p3.log 2>&1
 ncu --set full --clock-control none -k regex:k_write_prefill -s 1 -c 1 -o $O/prof_scatter python tools/time_scatter.py > $O/p4.log 2>&1
 ls -la $O
