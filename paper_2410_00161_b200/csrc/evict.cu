@@ -1523,8 +1523,8 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
   if (threadIdx.x == 0) { cnt_s[0] = 0; cnt_s[1] = 0; cnt_s[2] = 0; }
   __syncthreads();
   int32_t evk = 0;
-  auto block_flags = [&](int bl, uint32_t &masked_bits, uint32_t &live_bits) {
-    const int64_t f0 = (int64_t)tab[bl] * 16;
+  auto block_flags_at = [&](int bl, int32_t blk, uint32_t &masked_bits, uint32_t &live_bits) {
+    const int64_t f0 = (int64_t)blk * 16;
     const uint4 *kp = reinterpret_cast<const uint4 *>(keys + (int64_t)bl * 16);
     const int4 *lp = reinterpret_cast<const int4 *>(p.logical + f0);
     masked_bits = 0;
@@ -1544,6 +1544,9 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
         live_bits |= (lv[i] >= 0 ? 1u : 0u) << o;
       }
     }
+  };
+  auto block_flags = [&](int bl, uint32_t &masked_bits, uint32_t &live_bits) {
+    block_flags_at(bl, tab[bl], masked_bits, live_bits);
   };
   {
     int32_t carry = 0;
@@ -1575,20 +1578,24 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
     if (threadIdx.x == 0) cnt_s[0] = carry;
   }
   {
+    // (the table entry of a thread's next block is loaded a round ahead)
     int32_t carry = 0;
+    int32_t nxt = threadIdx.x < e ? tab[nb - 1 - threadIdx.x] : 0;
     for (int base = 0; base < e; base += NT) {
       const int t = base + threadIdx.x;
       const int bl = nb - 1 - t;  // descending blocks
+      const int32_t blk = nxt;
+      nxt = t + NT < e ? tab[nb - 1 - (t + NT)] : 0;
       uint32_t surv = 0;
       int64_t f0 = 0;
       if (t < e) {
         uint32_t mb, lb;
-        block_flags(bl, mb, lb);
+        block_flags_at(bl, blk, mb, lb);
         surv = ~mb & lb & 0xffffu;
         const int occ_n = C - bl * 16;
         const uint32_t occ_bits = occ_n >= 16 ? 0xffffu : occ_n <= 0 ? 0u : ((1u << occ_n) - 1u);
         evk += __popc(mb & occ_bits);
-        f0 = (int64_t)tab[bl] * 16;
+        f0 = (int64_t)blk * 16;
       }
       int32_t excl, tot;
       Scan(stmp).ExclusiveSum(__popc(surv), excl, tot);
