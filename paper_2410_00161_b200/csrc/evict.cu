@@ -287,7 +287,7 @@ __device__ bool load_body(const kvc_pool &p, const int32_t *rows, const int64_t 
   if (threadIdx.x == 0) shield_s = 0;
   __syncthreads();
   int shield = 0;
-  if (b == 16) {
+  if (b == 16 && NT >= 512) {
     // one thread per 16-slot block (64 B metric, 16 B flags in, 64 B keys
     // out); the table entry of the thread's next block is loaded a round
     // ahead, so each round waits for one load latency, not two
@@ -353,6 +353,41 @@ __device__ bool load_body(const kvc_pool &p, const int32_t *rows, const int64_t 
           kp[q] = make_uint4(kq[0], kq[1], kq[2], kq[3]);
         }
         if (with_hist && run) atomicAdd(&hist[cur], run);
+      }
+    }
+  } else if (b == 16) {
+    // short heads (many CTAs: registers matter more than latency hiding)
+    for (int64_t base = 0; base < nb; base += NT) {
+      const int64_t bl = base + threadIdx.x;
+      const bool in = bl < nb;
+      uint32_t kk[16];
+      if (in) {
+        const int64_t f0 = (int64_t)tab[bl] * 16;
+        const float4 *mp = reinterpret_cast<const float4 *>(p.metric + f0);
+        const uint4 pr = *reinterpret_cast<const uint4 *>(p.protected_ + f0);
+        const uint4 fr = *reinterpret_cast<const uint4 *>(p.fresh + f0);
+        const uint32_t pw[4] = {pr.x | fr.x, pr.y | fr.y, pr.z | fr.z, pr.w | fr.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 mv = mp[q];
+          const float mf[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int o = q * 4 + e;
+            const int64_t pos = bl * 16 + o;
+            const bool occ = pos < C;
+            const bool sh = occ && ((pw[q] >> (8 * e)) & 0xff);
+            shield += sh ? 1 : 0;
+            kk[o] = !occ ? f32_order_key(0.f) : sh ? kKeyInf : f32_order_key(mf[e]);
+          }
+        }
+        uint4 *kp = reinterpret_cast<uint4 *>(keys + bl * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kp[q] = make_uint4(kk[4 * q], kk[4 * q + 1], kk[4 * q + 2], kk[4 * q + 3]);
+      }
+      if (with_hist) {
+#pragma unroll
+        for (int o = 0; o < 16; ++o) hist_add(hist, in ? kk[o] >> 21 : 0, in);
       }
     }
   } else {
@@ -510,18 +545,22 @@ __device__ void bounds_body(const kvc_pool &p, const int32_t *rows, EvictState &
   const int si = g / S.hp, hi = g % S.hp;
   if (S.E[si] > 0) bounds_counts<NT>(p, rows, S, g, si, hi);
   else if (threadIdx.x == 0) { S.lo[g] = 0; S.hi[g] = 0; }
-  if (!last_of_sequence(S, si)) return;
-  select_seq<NT>(S, si, bsz, evict, move_off, p.status);
-  __shared__ int last_all;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int prev;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(S.done_all) : "memory");
-    last_all = prev == n_seqs - 1;
-    if (last_all) *S.done_all = 0;
-  }
-  __syncthreads();
-  if (last_all) offsets_all<NT>(S, n_seqs, move_off);
+}
+
+// (8) short heads (the decode-time batch of thousands of heads): the tie
+// rows of each sequence and the global move offsets in two small grids, so
+// the many-CTA k_bounds stays lean (registers, shared memory, occupancy).
+__global__ void __launch_bounds__(1024) k_select(EvictState S, int bsz, int32_t *evict, int64_t *move_off,
+                                                int32_t *status) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  select_seq<1024>(S, blockIdx.x, bsz, evict, move_off, status);
+}
+
+__global__ void __launch_bounds__(1024) k_offsets(EvictState S, int n_seqs, int64_t *move_off) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  offsets_all<1024>(S, n_seqs, move_off);
 }
 
 template <int NT>
@@ -834,7 +873,21 @@ __device__ void offsets_all(EvictState &S, int n_seqs, int64_t *move_off) {
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  for (int64_t g = threadIdx.x; g < T; g += NT) move_off[g] = __ldcg(move_off + g) + S.seq_moves[g / S.hp];
+  // eight independent loads in flight per thread (a decode round has
+  // thousands of heads)
+  for (int64_t g0 = threadIdx.x; g0 < T; g0 += 8 * NT) {
+    int64_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t g = g0 + (int64_t)u * NT;
+      v[u] = g < T ? __ldcg(move_off + g) + S.seq_moves[g / S.hp] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t g = g0 + (int64_t)u * NT;
+      if (g < T) move_off[g] = v[u];
+    }
+  }
   if (threadIdx.x == 0) move_off[T] = carry;
 }
 
@@ -2479,6 +2532,9 @@ int run_schedule(const kvc_pool *pool, const kvc_evict_args *a, EvictState &S, c
                a->clamped);
     launch_pdl(k_bounds<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, S, a->n_seqs, pool->block_size,
                a->evict, a->move_offsets);
+    launch_pdl(k_select, dim3((unsigned)a->n_seqs), dim3(1024), 0, s, S, pool->block_size, a->evict,
+               a->move_offsets, pool->status);
+    launch_pdl(k_offsets, dim3(1), dim3(1024), 0, s, S, a->n_seqs, a->move_offsets);
   } else {
     constexpr int NT = kThreads;
     launch_pdl(k_load<NT>, dim3((unsigned)T), dim3(NT), 0, s, *pool, a->seq_rows, a->budgets, S, 1, a->clamped);
