@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(256) k_copy_published(kvc_pool p, EvictState S
           int c = u - j * cm;
           uint4 *base = c >= vec ? vc : kc;
           c -= c >= vec ? vec : 0;
-          val[i] = __ldcs(base + (int64_t)src * vec + c);
+          val[i] = __ldg(base + (int64_t)src * vec + c);  // read-only path: no K/V is written meanwhile
           dst[i] = base + (int64_t)dd * vec + c;
         }
       }
