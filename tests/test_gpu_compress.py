@@ -176,12 +176,15 @@ def test_llama_slice_exact():
     assert got["freed_blocks"] == E
 
 
-@pytest.mark.parametrize("L,E_div", [(12000, 8), (9000, 3)])
-def test_long_heads_exact(L, E_div):
+@pytest.mark.parametrize("L,E_div,d", [(12000, 8, 64), (9000, 3, 64), (9000, 4, 128), (8500, 2, 256)])
+def test_long_heads_exact(L, E_div, d):
     """Heads longer than 8192 slots take the wide-CTA kernels (prefill-sized
-    heads); shorter ones the 256-thread kernels every other test covers."""
-    rng = np.random.default_rng(L)
-    b, d, layers, heads = 16, 64, 1, 3
+    heads: K3's last-level bounds, k_compact16 and the concurrent K/V copy
+    kernel, whose 16-byte units map to 1, 2 or 4 lanes' worth of a move at
+    head_dim 256 / 128 / 64); shorter ones the 256-thread kernels every
+    other test covers."""
+    rng = np.random.default_rng(L + d)
+    b, layers, heads = 16, 1, 3
     nblocks = layers * heads * (-(-L // b)) + 64
     st = O.OracleState(nblocks, b, d, layers, heads)
     O.alloc_prefill(st, 0, L)
