@@ -16,7 +16,7 @@ import torch
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkvc.so")
+LIB_PATH = os.environ.get("KVC_LIB_PATH") or os.path.join(_HERE, "libkvc.so")  # (override: experiments)
 
 KVC_FREE_TILE = 1024
 

@@ -1682,32 +1682,33 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
   const int keep = rb;
   const int Cn = C < keep * 16 ? C : keep * 16;
   {
-    for (int k0 = gtid; k0 < nmoves; k0 += 4 * GT) {  // four moves' loads in flight per thread
-      int64_t src[4], dst[4];
-      float mt[4];
-      int32_t lg[4];
-      uint8_t pr[4], fr[4];
+    constexpr int MU = 8;  // moves' loads in flight per thread
+    const int2 *mv2 = reinterpret_cast<const int2 *>(mv);
+    for (int k0 = gtid; k0 < nmoves; k0 += MU * GT) {
+      int2 sd[MU];
+      float mt[MU];
+      int32_t lg[MU];
+      uint8_t pr[MU], fr[MU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < MU; ++u) {
         const int k = k0 + u * GT;
-        src[u] = k < nmoves ? mv[2 * k] : -1;
-        dst[u] = k < nmoves ? mv[2 * k + 1] : -1;
+        sd[u] = k < nmoves ? mv2[k] : make_int2(-1, -1);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (src[u] >= 0) {
-          mt[u] = p.metric[src[u]];
-          lg[u] = p.logical[src[u]];
-          pr[u] = p.protected_[src[u]];
-          fr[u] = p.fresh[src[u]];
+      for (int u = 0; u < MU; ++u)
+        if (sd[u].x >= 0) {
+          mt[u] = p.metric[sd[u].x];
+          lg[u] = p.logical[sd[u].x];
+          pr[u] = p.protected_[sd[u].x];
+          fr[u] = p.fresh[sd[u].x];
         }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (src[u] >= 0) {
-          p.metric[dst[u]] = mt[u];
-          p.logical[dst[u]] = lg[u];
-          p.protected_[dst[u]] = pr[u];
-          p.fresh[dst[u]] = fr[u];
+      for (int u = 0; u < MU; ++u)
+        if (sd[u].x >= 0) {
+          p.metric[sd[u].y] = mt[u];
+          p.logical[sd[u].y] = lg[u];
+          p.protected_[sd[u].y] = pr[u];
+          p.fresh[sd[u].y] = fr[u];
         }
     }
     group_sync(bar, GT);
