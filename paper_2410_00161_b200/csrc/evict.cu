@@ -994,7 +994,10 @@ __device__ void publish_moves(const EvictState &S, int64_t h, int nm) {
   __threadfence();
   for (int c = threadIdx.x; c < nch; c += NT) {
     const unsigned long long v = ((unsigned long long)(h + 1) << 32) | (unsigned)c;
-    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(S.chunks + base_s + c), "l"(v) : "memory");
+    if (base_s + c < S.max_chunks)  // (sized from moves_capacity: a short buffer is a caller error)
+      asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(S.chunks + base_s + c), "l"(v) : "memory");
+    else
+      set_status(S.status, KVC_DEV_CAPACITY, (int32_t)h, base_s + c);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
