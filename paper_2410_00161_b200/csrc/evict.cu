@@ -1024,8 +1024,9 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 // exhausted, or after a 2 s wait: a head never published).
 __device__ __forceinline__ unsigned long long wait_chunk(const EvictState &S, const kvc_pool &p, int id, int T,
                                                          unsigned long long t0) {
+  if (id >= S.max_chunks) return 0;  // beyond the queue (publish flagged any overflow)
   for (int spin = 0;; ++spin) {
-    const unsigned long long d = id < S.max_chunks ? ld_acquire64(S.chunks + id) : 0;
+    const unsigned long long d = ld_acquire64(S.chunks + id);
     if (d) return d;
     if (ld_acquire(S.pub_count) == T && id >= __ldcg(S.chunk_tail)) return 0;  // all published, no more work
     if ((spin & 63) == 63) {
