@@ -55,6 +55,9 @@ void launch_pdl(void (*fn)(P...), dim3 grid, dim3 block, size_t smem, cudaStream
   cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
 }
 
+#ifndef KVC_CW_MINB
+#define KVC_CW_MINB 4
+#endif
 #ifndef KVC_C16_REGS
 #define KVC_C16_REGS 64  // two 512-thread CTAs per SM
 #endif
@@ -427,7 +430,7 @@ __device__ bool load_body(const kvc_pool &p, const int32_t *rows, const int64_t 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
+__global__ void __launch_bounds__(NT, NT <= 256 ? 8 : 2) k_load(kvc_pool p, const int32_t *rows, const int64_t *req,
                                                   EvictState S, int with_hist, int64_t *clamped) {
   grid_dep_wait();
   grid_dep_trigger();
@@ -517,7 +520,7 @@ __device__ bool hist_body(const kvc_pool &p, const int32_t *rows, EvictState &S,
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
+__global__ void __launch_bounds__(NT, NT <= 256 ? 8 : 2) k_hist(kvc_pool p, const int32_t *rows, EvictState S, int shift_hi,
                                                   int shift, int bits, const int64_t *req, int level,
                                                   int64_t *clamped) {
   grid_dep_wait();
@@ -1927,7 +1930,7 @@ __device__ void warp_sort(unsigned long long *a, int cnt, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kWC * 32, 4) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
+__global__ void __launch_bounds__(kWC * 32, KVC_CW_MINB) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
                                                           MoveArgs M, int64_t T_heads) {
   grid_dep_wait();
   grid_dep_trigger();
