@@ -171,16 +171,26 @@ __device__ void scan_hist(int32_t *hist) {
 // (counts are < 2^31: one head's slots).
 template <int NT>
 __device__ void add_contrib(const int32_t *cum, int32_t base, int cap, int b, int32_t *R, int nbins) {
-  for (int c = threadIdx.x; c < nbins; c += NT) {
-    // delta form: bin 0 carries the absolute value, later bins the increase
-    int32_t z = (base + cum[c]) / b;
-    if (z > cap) z = cap;
-    int32_t a = 0;
-    if (c > 0) {
-      a = (base + cum[c - 1]) / b;
-      if (a > cap) a = cap;
-    }
+  // each thread takes nbins / NT consecutive bins (the delta of bin c needs
+  // the row count of bin c - 1: one division per bin, none for the bins
+  // whose cumulative count does not move); b is a power of two in practice
+  const int per = nbins / NT;
+  const int sh = (b & (b - 1)) == 0 ? __ffs(b) - 1 : -1;
+  auto rows = [&](int32_t x) {
+    const int32_t z = sh >= 0 ? x >> sh : x / b;
+    return z > cap ? cap : z;
+  };
+  const int c0 = threadIdx.x * per;
+  int32_t prev_cum = c0 > 0 ? cum[c0 - 1] : -1;
+  int32_t a = c0 > 0 ? rows(base + prev_cum) : 0;
+  for (int i = 0; i < per; ++i) {
+    const int c = c0 + i;
+    const int32_t cc = cum[c];
+    if (cc == prev_cum) continue;  // empty bin: the row count stays
+    const int32_t z = rows(base + cc);
     if (z > a) atomicAdd(&R[c], z - a);
+    a = z;
+    prev_cum = cc;
   }
 }
 
