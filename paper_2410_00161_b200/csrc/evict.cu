@@ -55,9 +55,6 @@ void launch_pdl(void (*fn)(P...), dim3 grid, dim3 block, size_t smem, cudaStream
   cudaLaunchKernelEx(&cfg, fn, std::forward<A>(args)...);
 }
 
-#ifndef KVC_CW_MINB
-#define KVC_CW_MINB 4
-#endif
 #ifndef KVC_C16_REGS
 #define KVC_C16_REGS 64  // two 512-thread CTAs per SM
 #endif
@@ -1940,7 +1937,7 @@ __device__ void warp_sort(unsigned long long *a, int cnt, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kWC * 32, KVC_CW_MINB) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
+__global__ void __launch_bounds__(kWC * 32, 4) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
                                                           MoveArgs M, int64_t T_heads) {
   grid_dep_wait();
   grid_dep_trigger();
