@@ -41,7 +41,8 @@ L = ["# Round 2 — measurements on B200 (one GPU)", "",
      f"| clocks | median {b['clocks']['sm_mhz']} MHz, reasons {b['clocks']['reasons']} |", ""]
 
 rows = []
-for f in sorted(glob.glob(os.path.join(HERE, "configs", "*.json"))):
+keyed = []
+for f in glob.glob(os.path.join(HERE, "configs", "*.json")):
     try:
         lines = open(f).read().strip().splitlines()
         c = json.loads(lines[-1])
@@ -51,10 +52,13 @@ for f in sorted(glob.glob(os.path.join(HERE, "configs", "*.json"))):
     p = e.get("per_sequence_ms", {})
     r = e.get("ratio_to_decode_step", {})
     cf = c["config"]
-    rows.append(f"| {cf.get('preset')} | {cf.get('batch_per_gpu')} | {cf.get('context')} | {cf.get('compression')} | "
+    keyed.append(((cf.get('preset'), float(str(cf.get('compression')).rstrip('x') or 0), cf.get('context'),
+                   cf.get('batch_per_gpu')),
+                  f"| {cf.get('preset')} | {cf.get('batch_per_gpu')} | {cf.get('context')} | {cf.get('compression')} | "
                 f"{c['value']:,.0f} | {c['ms_per_step']:.3f} | {c['roofline']['frac'] * 100:.1f}% | "
                 f"{p.get('k2_window_metric', 0):.3f} | {p.get('k3k4_schedule_compact', 0):.3f} | "
-                f"{r.get('raw_without_k2', 0) * 100:.1f}% | `{os.path.basename(f)}` |")
+                f"{r.get('raw_without_k2', 0) * 100:.1f}% | `{os.path.basename(f)}` |"))
+rows = [r for _, r in sorted(keyed)]
 L += ["## BASELINE configs and the batch sweep (`tools/run_configs.sh` -> `profiles/configs/`)", "",
       "| preset | B/GPU | context | rate | decode tok/s | ms/step | K1 % of copy peak | K2 ms/seq | K3+K4 ms/seq | "
       "K3+K4 / step | file |", "|---|---|---|---|---|---|---|---|---|---|---|"] + rows + [""]
