@@ -30,11 +30,16 @@ GOLDEN = {c["name"]: c["records"] for c in CASES_JSON}
 GOLDEN_SHARDS = {c["name"]: c["shards"] for c in CASES_JSON}
 
 
+@pytest.mark.parametrize("graph_after", [0, None], ids=["graph-every-step", "graph-stable-batches"])
 @pytest.mark.parametrize("name,kw,reqs", CASES, ids=[c[0] for c in CASES])
-def test_engine_matches_reference(name, kw, reqs):
+def test_engine_matches_reference(name, kw, reqs, graph_after):
+    """graph_after=0: every decode step replays a CUDA graph (captured anew
+    whenever the batch changes); None: the default (graphs for batches
+    stable for a few steps, eager otherwise)."""
     cfg = K.AttentionConfig(SHAPE["n_q"], SHAPE["n_k"], SHAPE["d"], SHAPE["layers"])
+    extra = {} if graph_after is None else {"graph_after": graph_after}
     eng = K.Engine(cfg, K.MetricConfig(), make_policy(K, kw["policy"]), kw["num_blocks"], SHAPE["block_size"],
-                   rate=kw["rate"], budget_floor=kw["budget_floor"], record_schedules=True)
+                   rate=kw["rate"], budget_floor=kw["budget_floor"], record_schedules=True, **extra)
     for i, (pl, ot) in enumerate(reqs):
         eng.submit(HashTokens(1000 + i, pl, ot, SHAPE["layers"], SHAPE["n_q"], SHAPE["n_k"], SHAPE["d"]))
     got = [r.to_dict() for r in eng.run_to_completion()]

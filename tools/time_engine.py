@@ -24,9 +24,10 @@ REQS = [(int(rng.integers(512, 1536)), 64) for _ in range(32)]
 NUM_BLOCKS = 2400
 
 
-def run(mod, eng_mod):
+def run(mod, eng_mod, **kw):
     cfg = mod.AttentionConfig(NQ, NK, D, LAYERS)
-    eng = eng_mod.Engine(cfg, mod.MetricConfig(), eng_mod.POLICY_PRESETS["prefill-preempt"], NUM_BLOCKS, B, rate=8.0)
+    eng = eng_mod.Engine(cfg, mod.MetricConfig(), eng_mod.POLICY_PRESETS["prefill-preempt"], NUM_BLOCKS, B, rate=8.0,
+                         **kw)
     for i, (pl, ot) in enumerate(REQS):
         eng.submit(HashTokens(2000 + i, pl, ot, LAYERS, NQ, NK, D))
     t0 = time.perf_counter()
@@ -50,4 +51,5 @@ else:
     import paper_2410_00161_b200 as K
     run(K, K)  # warm-up (kernel attributes, tensor maps, allocator)
     out["device"] = run(K, K)
+    out["device_eager_decode"] = run(K, K, decode_graph=False)
 print(json.dumps(out))
