@@ -49,7 +49,8 @@
 extern "C" {
 #endif
 
-#define KVC_ABI_VERSION 2 /* 2: kvc_decode_args.early_pull; queue int32[2 + batch*heads] */
+#define KVC_ABI_VERSION 3 /* 2: kvc_decode_args.early_pull; queue int32[2 + batch*heads]
+                            3: kvc_window_args.write_k, kvc_write_prefill_v_layers */
 #define KVC_FREE_TILE 1024 /* blocks per free-count tile */
 
 typedef enum kvc_status {
@@ -159,6 +160,14 @@ int kvc_write_prefill_kv_layers(const kvc_pool *pool, int32_t seq_row, int32_t l
                                 int32_t n_layers, const void *k, const void *v, int32_t L,
                                 void *stream);
 
+/* Companion of kvc_window_metric with write_k = 1 (the K2 pass stores the K
+ * rows of the whole 16-key blocks): every V row, and the K rows of each
+ * head's partial last block; C := L.  Same layout as
+ * kvc_write_prefill_kv_layers. */
+int kvc_write_prefill_v_layers(const kvc_pool *pool, int32_t seq_row, int32_t layer,
+                               int32_t n_layers, const void *k, const void *v, int32_t L,
+                               void *stream);
+
 /* Install prompt metrics for one (row, layer): metrics f32 [heads][L],
  * protected u8 [L] (nullable = none); logical := position, fresh := 0. */
 int kvc_write_prompt_pass(const kvc_pool *pool, int32_t seq_row, int32_t layer,
@@ -241,6 +250,12 @@ typedef struct kvc_window_args {
   int64_t q_layer_stride;
   int64_t k_layer_stride;
   int64_t out_layer_stride;
+  /* 1 (with seq_row >= 0, block_size 16): the kernel also stores the prompt K
+   * rows of every whole 16-key block into the pool's k_cache through the
+   * tables, from the tiles it streams anyway (the prompt's K is read once);
+   * pair it with kvc_write_prefill_v_layers.  KVC_ERR_UNSUPPORTED (nothing
+   * done) on shapes that take the per-layer kernels. */
+  int32_t write_k;
 } kvc_window_args;
 
 int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *args, void *stream);

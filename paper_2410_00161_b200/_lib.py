@@ -63,7 +63,7 @@ class WindowArgs(ctypes.Structure):
         ("seq_row", _i32), ("layer", _i32), ("num_query_heads", _i32), ("L", _i32),
         ("q_win", _p), ("k", _p), ("window", _i32), ("pool", _i32), ("aggregation", _i32),
         ("protect_window", _i32), ("metrics_out", _p), ("n_layers", _i32), ("q_layer_stride", _i64),
-        ("k_layer_stride", _i64), ("out_layer_stride", _i64),
+        ("k_layer_stride", _i64), ("out_layer_stride", _i64), ("write_k", _i32),
     ]
 
 
@@ -109,6 +109,7 @@ _SIGS = {
     "kvc_append_kv": ([_p, _p, _p, _p, _i32, _i32, _p], _i32),
     "kvc_write_prefill_kv": ([_p, _i32, _i32, _p, _p, _i32, _p], _i32),
     "kvc_write_prefill_kv_layers": ([_p, _i32, _i32, _i32, _p, _p, _i32, _p], _i32),
+    "kvc_write_prefill_v_layers": ([_p, _i32, _i32, _i32, _p, _p, _i32, _p], _i32),
     "kvc_write_prompt_pass": ([_p, _i32, _i32, _p, _i64, _p, _i32, _p], _i32),
     "kvc_paged_decode": ([_p, _p, _p], _i32),
     "kvc_decode_scratch_bytes": ([_p, _i32, _i32, _i32], _i64),

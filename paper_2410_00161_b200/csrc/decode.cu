@@ -536,8 +536,10 @@ __global__ void k_clear_fresh_rows(kvc_pool p, const int32_t *rows, int n_rows) 
 // K/V scatter of a prompt: a warp copies one table block (b rows, contiguous
 // on both sides: the prompt's rows [blk*b, blk*b + b) and the pool block),
 // 16 bytes per lane, four chunks in flight; 32-bit index math per block.
+// k_tail_only: V rows, and K rows of the partial last block only (K2 with
+// write_k stores the whole blocks' K rows).
 __global__ void __launch_bounds__(256) k_write_prefill_kv(kvc_pool p, int row, int layer0, const uint4 *k,
-                                                          const uint4 *v, int L) {
+                                                          const uint4 *v, int L, int k_tail_only) {
   const int head = blockIdx.y;
   const int layer = layer0 + blockIdx.z;
   k += (int64_t)blockIdx.z * gridDim.y * L * (p.head_dim / 8);  // [layer][heads][L][d]
@@ -557,17 +559,24 @@ __global__ void __launch_bounds__(256) k_write_prefill_kv(kvc_pool p, int row, i
     const int n = rows * vec;  // chunks of this block
     const uint4 *sk = ks + (int64_t)bl * b * vec, *sv = vs + (int64_t)bl * b * vec;
     const int64_t d0 = (int64_t)tab[bl] * b * vec;
+    const bool with_k = !k_tail_only || rows < b;
     for (int c0 = 0; c0 < n; c0 += 4 * 32) {
       uint4 tk[4], tv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = c0 + u * 32 + lane;
-        if (c < n) { tk[u] = __ldcs(sk + c); tv[u] = __ldcs(sv + c); }
+        if (c < n) {
+          if (with_k) tk[u] = __ldcs(sk + c);
+          tv[u] = __ldcs(sv + c);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = c0 + u * 32 + lane;
-        if (c < n) { kc[d0 + c] = tk[u]; vc[d0 + c] = tv[u]; }
+        if (c < n) {
+          if (with_k) kc[d0 + c] = tk[u];
+          vc[d0 + c] = tv[u];
+        }
       }
     }
   }
@@ -694,8 +703,8 @@ int kvc_clear_fresh(const kvc_pool *pool, const int32_t *seq_rows, int32_t n_row
   return KVC_OK;
 }
 
-int kvc_write_prefill_kv_layers(const kvc_pool *pool, int32_t seq_row, int32_t layer, int32_t n_layers,
-                                const void *k, const void *v, int32_t L, void *stream) {
+static int write_prefill(const kvc_pool *pool, int32_t seq_row, int32_t layer, int32_t n_layers, const void *k,
+                         const void *v, int32_t L, void *stream, int k_tail_only) {
   if (!pool || !k || !v || L < 0 || n_layers < 1 || pool->head_dim % 8 != 0 || pool->block_size < 1)
     return KVC_ERR_INVALID;
   if (layer < 0 || layer + n_layers > pool->num_layers) return KVC_ERR_INVALID;
@@ -708,9 +717,20 @@ int kvc_write_prefill_kv_layers(const kvc_pool *pool, int32_t seq_row, int32_t l
   if (gx > cap) gx = cap;
   dim3 grid(gx, pool->num_kv_heads, n_layers);
   k_write_prefill_kv<<<grid, 256, 0, (cudaStream_t)stream>>>(*pool, seq_row, layer, (const uint4 *)k,
-                                                             (const uint4 *)v, L);
+                                                             (const uint4 *)v, L, k_tail_only);
   KVC_CHECK_LAUNCH();
   return KVC_OK;
+}
+
+int kvc_write_prefill_kv_layers(const kvc_pool *pool, int32_t seq_row, int32_t layer, int32_t n_layers,
+                                const void *k, const void *v, int32_t L, void *stream) {
+  return write_prefill(pool, seq_row, layer, n_layers, k, v, L, stream, 0);
+}
+
+int kvc_write_prefill_v_layers(const kvc_pool *pool, int32_t seq_row, int32_t layer, int32_t n_layers,
+                               const void *k, const void *v, int32_t L, void *stream) {
+  if (pool && pool->block_size != 16) return KVC_ERR_INVALID;  // pairs with K2's 16-key block stores
+  return write_prefill(pool, seq_row, layer, n_layers, k, v, L, stream, 1);
 }
 
 int kvc_write_prefill_kv(const kvc_pool *pool, int32_t seq_row, int32_t layer, const void *k, const void *v,

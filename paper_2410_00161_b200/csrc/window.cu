@@ -317,6 +317,7 @@ struct PersistParams {
   int64_t out_layer_stride;
   unsigned long long *trace;  // debug (KVC_K2_TRACE): [grid][nl][8] globaltimer stamps
   int dbg;                    // debug (KVC_K2_DBG): bit0 treat every tile as unmasked
+  int write_k;                // also store the prompt K rows of every whole 16-key block into the pool
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -327,7 +328,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 constexpr int kPEW = 8;                // epilogue warps
 constexpr int kPGroups = kPEW / 4;     // tile groups (4 warps cover the 4 TMEM lane quadrants)
-constexpr int kPThreads = 64 + 32 * kPEW;
+constexpr int kPThreads = 96 + 32 * kPEW;  // TMA, MMA, epilogue warps, K-row writer
 
 template <int D>
 constexpr int persist_stages() { return D >= 128 ? 5 : 10; }
@@ -425,7 +426,7 @@ __device__ __forceinline__ void epi_head_barrier(int *cnt, int target, bool lead
 template <int N, int D, bool RECOMP>
 __global__ void __launch_bounds__(kPThreads, 1)
     k_window_persist(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
-                     const PersistParams P) {
+                     const __grid_constant__ CUtensorMap tmP, const PersistParams P) {
   constexpr int kS = 512 / N;  // TMEM slots
   constexpr int kPasses = RECOMP ? 2 : 1;
   constexpr int kStages = persist_stages<D>();
@@ -456,7 +457,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int ntiles = t_hi - t_lo;  // >= 1; <= kS unless RECOMP (checked on the host)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    // write_k: a stage is free again once its MMAs have read it (tcgen05.commit) and
+    // its K-row stores have read it (the MMA warp's arrival after wait_group.read)
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], P.write_k ? 2 : 1); }
     for (int a = 0; a < kS; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
     for (int b = 0; b < 2; ++b) { mbar_init(&qfull[b], 1); mbar_init(&qempty[b], 1); }
     fence_barrier_init();
@@ -521,6 +524,56 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (P.trace && gi == kPasses * ntiles - 1) P.trace[((int64_t)blockIdx.x * P.nl + l) * 8 + 7] = gtimer();
         }
         __syncwarp();
+      }
+    }
+  } else if (warp == 2 + kPEW) {
+    // ---------------- K-row writer (write_k: the unfused prefill) ----------------
+    // Each staged K tile also goes to the paged cache, one TMA store per
+    // (16-key block, 64-column atom), so the prompt's K is read from HBM once
+    // for the metric and the write.  Lane b < 8 holds block b's pool id of
+    // the current tile, loaded a tile ahead (-1: recompute pass, or a block
+    // not whole inside the prompt: the scatter writes that one).  A stage is
+    // released (its second arrival) once its stores have read it.
+    if (P.write_k) {
+      const uint32_t gtot = (uint32_t)(P.nl * kPasses * ntiles);
+      auto tile_blk = [&](uint32_t g) -> int32_t {
+        const int l = (int)(g / (uint32_t)(kPasses * ntiles)), gi = (int)(g % (uint32_t)(kPasses * ntiles));
+        if (gi >= ntiles || lane >= kTileKeys / 16) return -1;
+        const int key0 = (t_lo + gi) * kTileKeys + lane * 16;
+        if (key0 + 16 > P.L) return -1;
+        return head_table(P.p, head_index(P.p, P.row, P.layer0 + l, head))[key0 / 16];
+      };
+      int32_t blk_nxt = tile_blk(0);
+      int prev_s = -1;
+      for (uint32_t g = 0; g < gtot; ++g) {
+        const int s = g % kStages;
+        const int32_t blk_cur = blk_nxt;
+        blk_nxt = g + 1 < gtot ? tile_blk(g + 1) : -1;
+        int32_t blks[kTileKeys / 16];
+#pragma unroll
+        for (int b = 0; b < kTileKeys / 16; ++b) blks[b] = __shfl_sync(0xffffffffu, blk_cur, b);
+        mbar_wait(&full[s], (g / kStages) & 1);
+        if (lane == 0) {
+          const uint8_t *tile = ktiles + s * kTileBytes;
+#pragma unroll
+          for (int b = 0; b < kTileKeys / 16; ++b)
+            if (blks[b] >= 0)
+#pragma unroll
+              for (int a = 0; a < kAtoms; ++a)
+                tma_store_3d(&tmP, tile + a * kTileKeys * 128 + b * 16 * 128, 0, blks[b] * 16, a);
+          bulk_commit();
+          if (prev_s >= 0) {  // the previous stage's stores have read it
+            bulk_wait_read<1>();
+            mbar_arrive(&empty[prev_s]);
+          }
+          prev_s = s;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        bulk_wait_read<0>();
+        if (prev_s >= 0) mbar_arrive(&empty[prev_s]);
+        bulk_wait<0>();  // the K rows are in the pool before the grid completes
       }
     }
   } else {
@@ -815,6 +868,20 @@ bool make_map3(CUtensorMap *map, const void *base, int64_t rows, int D, int box_
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The pool as {64 elems, rows = blocks * 16, D/64 atoms}, box {64, 16, 1}
+// SWIZZLE_128B: one 16-row, 64-column slice of a staged K tile per store.
+bool make_pool_store_map(CUtensorMap *map, const void *base, int64_t rows, int D) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(D / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
+  cuuint32_t box[3] = {64, 16, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap *map, const void *base, int64_t rows, int D, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
@@ -859,9 +926,11 @@ int run_persist(const kvc_pool *pool, const kvc_window_args *a, const WinParams 
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPThreads, smem);
   if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
-  CUtensorMap tmK, tmQ;
+  CUtensorMap tmK, tmQ, tmP;
   if (!make_map3(&tmK, a->k, (int64_t)nl * W.H * W.L, D, kTileKeys)) return KVC_ERR_CUDA;
   if (!make_map(&tmQ, a->q_win, (int64_t)nl * a->num_query_heads * W.wq, D, N)) return KVC_ERR_CUDA;
+  tmP = tmK;  // unused unless write_k
+  if (a->write_k && !make_pool_store_map(&tmP, pool->k_cache, (int64_t)pool->num_blocks * 16, D)) return KVC_ERR_CUDA;
   PersistParams P;
   P.L = W.L; P.Lp = (W.L + 3) & ~3; P.H = W.H; P.RW = W.RW; P.wq = W.wq; P.start = W.start; P.nl = nl; P.n_q = a->num_query_heads;
   P.tiles_per_head = W.tiles_per_head; P.cph = cph;
@@ -874,6 +943,7 @@ int run_persist(const kvc_pool *pool, const kvc_window_args *a, const WinParams 
   P.out_layer_stride = a->out_layer_stride;
   P.trace = nullptr;
   P.dbg = getenv("KVC_K2_DBG") ? atoi(getenv("KVC_K2_DBG")) : 0;
+  P.write_k = a->write_k ? 1 : 0;
   static const bool trace = getenv("KVC_K2_TRACE") != nullptr;
   if (trace) cudaMalloc(&P.trace, (size_t)W.H * cph * nl * 8 * 8);
   cudaMemsetAsync(W.bar_cnt, 0, W.H * sizeof(int), s);
@@ -887,7 +957,7 @@ int run_persist(const kvc_pool *pool, const kvc_window_args *a, const WinParams 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const int rc = cudaLaunchKernelEx(&cfg, fn, tmK, tmQ, P) == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
+  const int rc = cudaLaunchKernelEx(&cfg, fn, tmK, tmQ, tmP, P) == cudaSuccess ? KVC_OK : KVC_ERR_CUDA;
   if (trace) {
     // debug: per layer, average over CTAs of each phase's duration (us), relative to the CTA's A start
     const int G = W.H * cph;
@@ -1018,13 +1088,15 @@ extern "C" int kvc_window_metric(const kvc_pool *pool, const kvc_window_args *a,
   // persistent kernel over all layers when the layers are packed back to back
   const bool packed = nl == 1 || (a->k_layer_stride == (int64_t)H * a->L * D &&
                                   a->q_layer_stride == (int64_t)a->num_query_heads * P.wq * D);
+  if (a->write_k && (a->seq_row < 0 || !pool->k_cache || pool->block_size != 16 || twopass || !packed || D > 128))
+    return KVC_ERR_UNSUPPORTED;
   if (!twopass && packed && D <= 128) {
     int rc = KVC_ERR_UNSUPPORTED;
     if (N == 32 && D == 64) rc = run_persist<32, 64>(pool, a, P, nl, s);
     else if (N == 32 && D == 128) rc = run_persist<32, 128>(pool, a, P, nl, s);
     else if (N == 64 && D == 64) rc = run_persist<64, 64>(pool, a, P, nl, s);
     else if (N == 64 && D == 128) rc = run_persist<64, 128>(pool, a, P, nl, s);
-    if (rc != KVC_ERR_UNSUPPORTED) return rc;
+    if (rc != KVC_ERR_UNSUPPORTED || a->write_k) return rc;  // write_k: the per-layer kernels do not store K
   }
   // otherwise one layer at a time, two passes: the layer's K (64 MB at
   // Llama-8B shapes) stays in L2 between the statistics and the metric pass

@@ -32,9 +32,14 @@ def _dev_bf16(x, dev) -> torch.Tensor:
 
 
 def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev, pool_p=None,
-                 seq_row: int = -1, layer: int = 0, metrics_out=None) -> None:
+                 seq_row: int = -1, layer: int = 0, metrics_out=None, write_k: bool = False) -> bool:
     """K2 for one layer (q (n_q, L|w', d), k (H, L, d)) or several consecutive
-    layers (q (l, n_q, L|w', d), k (l, H, L, d)) in one C call."""
+    layers (q (l, n_q, L|w', d), k (l, H, L, d)) in one C call.
+
+    write_k: the kernel also stores the K rows of every whole 16-key block
+    into the cache (the prompt's K read once for the metric and the write).
+    Returns False, with nothing done, when the shape takes the per-layer
+    kernels, which cannot (the caller then scatters K itself)."""
     multi = k.dim() == 4
     if not multi:
         q, k = q[None], k[None]
@@ -63,6 +68,7 @@ def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev,
     a.q_layer_stride = q_win[0].numel()
     a.k_layer_stride = k[0].numel()
     a.out_layer_stride = metrics_out[0].numel() if metrics_out is not None else 0
+    a.write_k = int(bool(write_k))
     if pool_p is None:
         pool_p = _lib.KvcPool()
         pool_p.status = _lib.DeviceContext.get(dev).status.data_ptr()
@@ -70,8 +76,11 @@ def _window_call(q, k, cfg: MetricConfig, num_kv_heads: int, head_dim: int, dev,
     pool_p.head_dim = head_dim
     # raw [2][H][L] f32 + partials [H][<=304][<=64] float2 + barrier counters
     with_scratch(pool_p, dev, num_kv_heads * (2 * (L + 3) * 4 + 304 * 64 * 8 + 64) + (1 << 16))
-    _lib.check(_lib.lib().kvc_window_metric(ctypes.byref(pool_p), ctypes.byref(a), _lib.stream_ptr(dev)),
-               "window_metric")
+    rc = _lib.lib().kvc_window_metric(ctypes.byref(pool_p), ctypes.byref(a), _lib.stream_ptr(dev))
+    if write_k and rc == _lib.ERR_UNSUPPORTED:
+        return False
+    _lib.check(rc, "window_metric")
+    return True
 
 
 def window_metrics_qk(q, k, cfg: MetricConfig, num_kv_heads: int, device=None):
@@ -151,14 +160,17 @@ def write_prefill_kv(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, la
     tables.ctx_bound[row] = max(tables.ctx_bound[row], L)
 
 
-def write_prefill_kv_layers(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, k, v) -> None:
-    """Scatter every layer's prompt K/V (layers, heads, L, d) in one launch; C := L."""
+def write_prefill_kv_layers(cache: UnifiedKVCache, tables: BlockTables, seq_id: int, k, v,
+                            v_only: bool = False) -> None:
+    """Scatter every layer's prompt K/V (layers, heads, L, d) in one launch; C := L.
+    v_only: V, and K of each head's partial last block only (K2 with
+    write_k stored the whole blocks' K rows)."""
     dev = cache.device
     kt, vt = _dev_bf16(k, dev), _dev_bf16(v, dev)
     nl, L = kt.shape[0], kt.shape[2]
     p = pool_struct(cache=cache, tables=tables)
-    _lib.check(_lib.lib().kvc_write_prefill_kv_layers(ctypes.byref(p), tables.row(seq_id), 0, nl, kt.data_ptr(),
-                                                      vt.data_ptr(), L, _lib.stream_ptr(dev)),
+    fn = _lib.lib().kvc_write_prefill_v_layers if v_only else _lib.lib().kvc_write_prefill_kv_layers
+    _lib.check(fn(ctypes.byref(p), tables.row(seq_id), 0, nl, kt.data_ptr(), vt.data_ptr(), L, _lib.stream_ptr(dev)),
                "write_prefill_kv_layers")
     row = tables.row(seq_id)
     tables.ctx_bound[row] = max(tables.ctx_bound[row], L)
@@ -193,13 +205,21 @@ def prefill_sequence(cache: UnifiedKVCache, tables: BlockTables, manager: BlockM
         raise ValueError("the full metric needs every prompt query: q (l, n_q, L, d)")
     demand = manager.allocate_prefill(seq_id, L)
     kt, vt, qt = _dev_bf16(k, dev), _dev_bf16(v, dev), _dev_bf16(q, dev)
-    write_prefill_kv_layers(cache, tables, seq_id, kt, vt)
     if cfg.mode == FULL:
+        write_prefill_kv_layers(cache, tables, seq_id, kt, vt)
         _install_full(cache, tables, store, seq_id, qt, kt, cfg)
         return demand
+    # K2 streams the prompt's K anyway: it also stores the whole blocks' K
+    # rows, after the scatter has written V (+ each head's partial last K
+    # block) and set C := L, so K is read from HBM once instead of twice
     p = pool_struct(cache=cache, tables=tables, store=store)
-    _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
-                 seq_row=tables.row(seq_id), layer=0)
+    if tables.block_size == 16:
+        write_prefill_kv_layers(cache, tables, seq_id, kt, vt, v_only=True)
+        if _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p,
+                        seq_row=tables.row(seq_id), layer=0, write_k=True):
+            return demand
+    write_prefill_kv_layers(cache, tables, seq_id, kt, vt)  # shapes K2 cannot store K for
+    _window_call(qt, kt, cfg, tables.num_kv_heads, cache.head_dim, dev, pool_p=p, seq_row=tables.row(seq_id), layer=0)
     return demand
 
 

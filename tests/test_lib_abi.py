@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.kvc_abi_version() == 2
+    assert lib.kvc_abi_version() == 3
     assert lib.kvc_status_name(1).decode() == "PreemptionNeeded"
 
 
