@@ -147,3 +147,41 @@ def test_fused_full_size_equals_unfused():
     assert live.numel() == layers * H * (L // 8)
     assert torch.equal(a.cache.keys_flat[live], b_.cache.keys_flat[live])
     assert torch.equal(a.cache.values_flat[live], b_.cache.values_flat[live])
+
+
+@pytest.mark.parametrize("layers,H,r,d,L", [(2, 2, 4, 64, 300), (2, 8, 4, 128, 4100), (1, 4, 8, 128, 1024),
+                                             (1, 8, 4, 64, 40000)])
+def test_prefill_reads_k_once_equals_scatter(layers, H, r, d, L):
+    """prefill_sequence's K2 stores the whole blocks' K rows from its staged
+    tiles (write_k; the scatter writes V and each head's partial last block):
+    the cache and slot state equal the plain K+V scatter followed by K2.  The
+    last shape runs K2's recompute mode (more tiles per CTA than TMEM slots),
+    where only the first pass stores."""
+    b = 16
+    g = torch.Generator(device="cuda")
+    g.manual_seed(L + d)
+    q = torch.randn((layers, H * r, 8, d), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((layers, H, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((layers, H, L, d), generator=g, device="cuda").to(torch.bfloat16)
+    nb = layers * H * (L // b + 2) + 16
+    rigs = []
+    for fused_k in (True, False):
+        rig = DevRig(nb, b, d, layers, H, max_seqs=2, max_blocks=L // b + 4)
+        if fused_k:
+            K.prefill_sequence(rig.cache, rig.tables, rig.manager, rig.store, 0, q, k, v, K.MetricConfig())
+        else:
+            rig.manager.allocate_prefill(0, L)
+            K.prefill.write_prefill_kv_layers(rig.cache, rig.tables, 0, k, v)
+            p = K.cache.pool_struct(cache=rig.cache, tables=rig.tables, store=rig.store)
+            K.prefill._window_call(q, k, K.MetricConfig(), H, d, rig.cache.device, pool_p=p,
+                                   seq_row=rig.tables.row(0), layer=0)
+        torch.cuda.synchronize()
+        _lib.DeviceContext.get(rig.cache.device).raise_status()
+        rigs.append(rig)
+    a, c = rigs
+    assert torch.equal(a.cache.keys, c.cache.keys)
+    assert torch.equal(a.cache.values, c.cache.values)
+    assert torch.equal(a.store.metrics_flat, c.store.metrics_flat)
+    assert torch.equal(a.store.logical_flat, c.store.logical_flat)
+    assert torch.equal(a.store.protected_flat, c.store.protected_flat)
+    assert torch.equal(a.tables.ctx, c.tables.ctx)
