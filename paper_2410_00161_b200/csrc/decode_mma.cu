@@ -40,14 +40,16 @@ constexpr int kBlk = 16;         // tokens per KV block
 constexpr int kHP = 8;           // heads per MMA (group padded to 8)
 constexpr int kItemBlocks = 16;  // max blocks per (warp) work item: 256 positions
 // Blocks per work item for a launch: 16 (256 positions) unless that leaves
-// fewer than two items per resident warp (small batches), then 8/4 - more,
+// fewer items than resident warps (small batches), then 8/4 - more,
 // shorter split-KV items (down to 4 blocks) at the cost of more partials to merge.
 static int item_blocks_for(int64_t pairs, int max_ctx) {
   static const int forced = getenv("KVC_K1_ITEM_BLOCKS") ? atoi(getenv("KVC_K1_ITEM_BLOCKS")) : 0;  // experiments
   if (forced >= 1 && forced <= kItemBlocks) return forced;
   const int64_t warps = 148 * 2 * 4;  // 2 CTAs x 4 warps per SM
   int ib = kItemBlocks;
-  while (ib > 4 && pairs * ((max_ctx + ib * kBlk - 1) / (ib * kBlk)) < 2 * warps) ib /= 2;
+  // (round 2: one item per resident warp is enough; B = 8 at 8 heads now
+  // takes 256-position items, 1.05 -> 1.03 ms per step)
+  while (ib > 4 && pairs * ((max_ctx + ib * kBlk - 1) / (ib * kBlk)) < warps) ib /= 2;
   return ib;
 }
 
