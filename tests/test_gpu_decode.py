@@ -41,7 +41,7 @@ def test_library_loads_with_every_symbol():
     from paper_2410_00161_b200 import _lib
 
     lib = _lib.load()
-    assert lib.kvc_abi_version() == 2
+    assert lib.kvc_abi_version() == 3
     for name in _lib.EXPORTED:
         assert hasattr(lib, name)
 
