@@ -800,6 +800,9 @@ def main():
     ev = eviction_rounds(S, args)
     populate(S, args)
     dec = decode_bench(S, args)
+    if os.environ.get("KVC_BENCH_DECODE_ONLY"):  # experiments: decode timing only
+        print("DECODE", {k: v for k, v in dec.items() if not hasattr(v, "shape")}, flush=True)
+        return
     if args.save_ctx and rank == 0:
         with open(ctx_fixture_path(args), "w") as fh:
             json.dump({"shape": [args.batch, args.layers, args.kv_heads], "context": args.context, "rate": args.rate,

@@ -80,6 +80,7 @@ struct Params {
   float *part_ml;   // [pairs][n_ck][2][kHP]
   float *part_o;    // [pairs][n_ck][r][D]
   unsigned long long *trace;  // debug (KVC_K1_TRACE): [grid*warps][2] start/end globaltimer
+  unsigned long long *trace_b;  // debug (KVC_K1_TRACE_PTR): kernel B [cta][2] after-wait/end globaltimer
 };
 
 // Programmatic dependent launch: the finish kernel (and the next stream) is launched
@@ -591,6 +592,11 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
   }
   pdl_wait();
   pdl_trigger();
+  if (P.trace_b && threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    P.trace_b[(blockIdx.y * gridDim.x + blockIdx.x) * 2] = t0;
+  }
   if (pair == 0 && slice == 0 && threadIdx.x == 0) *P.counter = 0;  // queue head for the next launch
   if (bad) set_status(p.status, KVC_DEV_NUMERIC, (int32_t)hidx, 0);
   if (cp < 1 || cp > cap || cp > P.max_ctx_pad) {  // no item ran (or not all of it) for this head
@@ -710,6 +716,11 @@ __global__ void __launch_bounds__(256) k_decode_finish(const Params P) {
       discard_l2(b0 + (int64_t)(i / lpc) * E4 * 16 + (int64_t)(i % lpc) * 128);
   }
   if (!P.metric_split) finish_metric(P, pair, slice, hidx, cp, c_old, append, Ms, iZ);
+  if (P.trace_b && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+    P.trace_b[(blockIdx.y * gridDim.x + blockIdx.x) * 2 + 1] = t1;
+  }
   // C += 1 once every CTA of the pair has read C (the last to arrive bumps;
   // k_decode_metric on the side stream runs after this kernel and sees C + 1)
   if (append) {
@@ -856,7 +867,10 @@ int launch(Params &P, cudaStream_t s) {
   auto fb = k_decode_finish<D>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // (fails if the kernel ever gains static shared memory: report it rather
+    // than fall back to the generic path silently on a 48 KB default)
+    if (cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return KVC_ERR_CUDA;
     cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     configured = true;
   }
@@ -885,7 +899,7 @@ int launch(Params &P, cudaStream_t s) {
     cfg.numAttrs = pdl_off() ? 0 : 1;
     cudaLaunchKernelEx(&cfg, fa, tmK, tmV, P);
   }
-  if (P.trace) {
+  if (P.trace && !P.trace_b) {
     // debug: spread of the warps' end times in this launch (synchronises)
     const int nw = grid * kNW;
     unsigned long long *h = (unsigned long long *)malloc((size_t)nw * 16);
@@ -1044,6 +1058,19 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
   off += (int64_t)a->batch * H * P.n_ck * 2 * kHP * 4;
   P.part_o = reinterpret_cast<float *>(base + off);
   P.trace = nullptr;
+  P.trace_b = nullptr;
+  {
+    // debug (KVC_K1_TRACE_PTR=<device address>, tools/trace_step.py):
+    // per-layer globaltimer slots [layer % 64][65536] u64 - kernel A warps
+    // at 0, kernel B CTAs at 32768 - set at capture time, so graph replays
+    // fill them
+    static const char *tp = getenv("KVC_K1_TRACE_PTR");
+    if (tp) {
+      unsigned long long *b = reinterpret_cast<unsigned long long *>(strtoull(tp, nullptr, 0));
+      P.trace = b + (int64_t)(a->layer % 64) * 65536;
+      P.trace_b = P.trace + 32768;
+    }
+  }
   {
     static int calls = 0;
     static unsigned long long *tbuf = nullptr;
