@@ -922,12 +922,17 @@ int launch(Params &P, cudaStream_t s) {
     if (smem_b > 64 * 1024) return KVC_ERR_UNSUPPORTED;
     const int pairs_b = P.batch * P.p.num_kv_heads;
     // small batches: several CTAs per (sequence, head) share the merge and
-    // the metric pass (round 2, inside the CUDA-graph step: 8 / 4 / 1 CTAs
-    // best at 8 / 64 / 256 pairs (B = 1 / 8 / 32 at 8 heads): B = 8 1.24 ->
-    // 1.06 ms and B = 32 3.26 -> 3.08 ms per step against the round-1 rule
-    // 512 / pairs; each CTA folds the head statistics itself)
+    // (without the side-stream metric kernel) the metric pass; each CTA
+    // folds the head statistics itself.  Eager: 256 / pairs, at most 8.
+    // With the metric on the side stream (the CUDA-graph step) kernel B only
+    // merges, and its CTAs hold registers the next layer's kernel A CTAs
+    // need to land (per-layer timeline: A's entries spread over the 4 us of
+    // B at 256 B CTAs): one CTA per pair from 16 pairs up - B = 2 / 4 / 8
+    // at 8 heads 0.59 / 0.67 / 1.03 -> 0.56 / 0.64 / 0.99 ms per step -,
+    // 8 for <= 8 pairs (B = 1: 0.45 vs 0.50 ms with 1)
     int ms = 256 / (pairs_b > 0 ? pairs_b : 1);
     ms = ms < 1 ? 1 : ms > 8 ? 8 : ms;
+    if (P.metric_split && pairs_b > 8) ms = 1;
     static const int ms_forced = getenv("KVC_K1_MSPLIT") ? atoi(getenv("KVC_K1_MSPLIT")) : 0;  // experiments
     if (ms_forced > 0) ms = ms_forced;
     launch_pdl(fb, pairs_b, 256, smem_b, s, P, ms);
