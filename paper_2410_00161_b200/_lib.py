@@ -238,3 +238,19 @@ class DeviceContext:
         if code == DEV_CAPACITY:
             raise E.DeviceCapacityError(f"head {a} needs {b} table entries")
         raise RuntimeError(f"device status {st}")
+
+
+def is_host_array(x) -> bool:
+    """True for a caller-side (non-torch) array: the reference-signature entry
+    points then return NumPy arrays like the reference does (computed on the
+    GPU, copied back); device tensors in give device tensors out."""
+    return not torch.is_tensor(x)
+
+
+def to_host(t: torch.Tensor):
+    """A device result as the reference's NumPy type (floats as float64)."""
+    t = t.detach()
+    if t.is_floating_point():
+        t = t.to(torch.float64)
+    return t.cpu().numpy()
+

@@ -129,7 +129,10 @@ def paged_attention(query, cache: UnifiedKVCache, tables: BlockTables, seq_id: i
     out = paged_decode(q, cache, tables, None, layer, cfg, out_f32=True, rows_out=rows,
                        rows_tensor=rt, host_rows=[row], max_ctx=cmax)
     _lib.DeviceContext.get(dev).raise_status()
-    return out[0], [rows[0, h, :, : ctx[h]] for h in range(cfg.num_kv_heads)]
+    res = out[0], [rows[0, h, :, : ctx[h]] for h in range(cfg.num_kv_heads)]
+    if _lib.is_host_array(query):  # NumPy in, NumPy out (the reference's types)
+        return _lib.to_host(res[0]), [_lib.to_host(x) for x in res[1]]
+    return res
 
 
 def dense_attention(q, k, v):
@@ -142,13 +145,16 @@ def dense_attention(q, k, v):
 def gqa_attention(q, k, v, cfg: AttentionConfig):
     """Dense causal grouped-query attention (attention.py:62-89): query head h
     reads KV head h // group_size.  q (n_q, L, d), k/v (n_k, L, d).  Returns
-    (out (n_q, L, d), attn (n_q, L, L)) as fp32 device tensors; the attention
+    (out (n_q, L, d), attn (n_q, L, L)) as fp32 device tensors (NumPy float64
+    arrays when q is a NumPy array, as the reference returns); the attention
     is row-stochastic and zero above the diagonal.  Materialises O(n_q L^2)
     like the reference; for prompt metrics at length use window_metrics_qk /
     full_metrics_qk, which never form it."""
     dev = _lib.require_cuda(q.device if torch.is_tensor(q) and q.is_cuda else None)
     f32 = lambda x: torch.as_tensor(np.asarray(x) if not torch.is_tensor(x) else x).to(dev, torch.float32).contiguous()
     qt, kt, vt = f32(q), f32(k), f32(v)
+    if not (torch.isfinite(qt).all() and torch.isfinite(kt).all() and torch.isfinite(vt).all()):
+        raise NumericError("non-finite values in attention inputs")
     if qt.shape[0] != cfg.num_query_heads or kt.shape[0] != cfg.num_kv_heads:
         raise ValueError("head counts do not match the attention config")
     if kt.shape != vt.shape or qt.shape[1:] != kt.shape[1:]:
@@ -157,7 +163,7 @@ def gqa_attention(q, k, v, cfg: AttentionConfig):
     out = torch.empty((n_q, L, d), dtype=torch.float32, device=dev)
     attn = torch.empty((n_q, L, L), dtype=torch.float32, device=dev)
     if L == 0:
-        return out, attn
+        return (_lib.to_host(out), _lib.to_host(attn)) if _lib.is_host_array(q) else (out, attn)
     a = _lib.DenseArgs()
     a.num_query_heads, a.L = n_q, L
     a.q, a.k, a.v, a.out, a.attn = qt.data_ptr(), kt.data_ptr(), vt.data_ptr(), out.data_ptr(), attn.data_ptr()
@@ -168,4 +174,6 @@ def gqa_attention(q, k, v, cfg: AttentionConfig):
     p.head_dim = d
     _lib.check(_lib.lib().kvc_gqa_attention(ctypes.byref(p), ctypes.byref(a), _lib.stream_ptr(dev)), "gqa_attention")
     ctx.raise_status()
+    if _lib.is_host_array(q):  # NumPy in, NumPy out (the reference's types)
+        return _lib.to_host(out), _lib.to_host(attn)
     return out, attn

@@ -1838,14 +1838,20 @@ __device__ void compact16_head(kvc_pool &p, const int32_t *rows, EvictState &S, 
 // ---------------------------------------------------------------------------
 // k_compact_warp: one warp per head for heads of at most 8192 slots (the
 // decode-time batch: thousands of short heads, a few evicted blocks each).
-// No CTA barriers; 8 heads per CTA, 4 KB of shared memory per warp.
+// No CTA barriers; one head per (one-warp) CTA, 4 KB of shared memory.
 //  * T_h and the tie cut come from the candidates (keys < T*, or the ties at
 //    T*) sorted by (key, secondary) in shared memory when there are at most
 //    kCand of them, else from a warp radix select over the head's keys.
 //  * holes / survivors / pairs / free / renumber as k_compact16, each pass
 //    one 16-slot block per lane with warp scans.
 // ---------------------------------------------------------------------------
-constexpr int kWC = 8;      // warps (heads) per CTA
+#ifndef KVC_CW_WARPS
+#define KVC_CW_WARPS 1
+#endif
+// warps (heads) per CTA.  One: a CTA retires with its head, so a short or
+// non-evicting head frees its slot at once (8 heads per CTA held each CTA
+// until its slowest head: 33% achieved occupancy; decode round -2%)
+constexpr int kWC = KVC_CW_WARPS;
 
 struct WarpArea {
   unsigned long long cand[kCand];  // composites (key << 32 | secondary); or a 256-bin histogram
@@ -1937,7 +1943,7 @@ __device__ void warp_sort(unsigned long long *a, int cnt, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kWC * 32, 4) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
+__global__ void __launch_bounds__(kWC * 32, 32 / kWC) k_compact_warp(kvc_pool p, const int32_t *rows, EvictState S,
                                                           MoveArgs M, int64_t T_heads) {
   grid_dep_wait();
   grid_dep_trigger();

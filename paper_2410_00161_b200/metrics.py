@@ -208,7 +208,8 @@ def window_metrics(attn, cfg: MetricConfig, num_kv_heads: int):
     """Observation-window metrics from an (n_q, L, L) causal attention tensor
     (metrics.py:68-89): f of the last ``cfg.window`` rows summed per key over
     the key's query group, max-pooled over keys.  Returns (metrics (H, L) fp32
-    device tensor, protected (L,) bool device tensor).  The serving path
+    device tensor, protected (L,) bool device tensor); NumPy arrays (float64,
+    bool) when attn is a NumPy array, as the reference returns.  The serving path
     (prefill_sequence, window_metrics_qk) computes the same from Q and K on
     tcgen05 without the attention tensor."""
     out = _attn_call(attn, cfg, num_kv_heads, 0)
@@ -217,13 +218,16 @@ def window_metrics(attn, cfg: MetricConfig, num_kv_heads: int):
     protected = torch.arange(L, device=out.device) >= start
     if not cfg.protect_window:
         protected[:] = False
+    if _lib.is_host_array(attn):  # NumPy in, NumPy out (the reference's types)
+        return _lib.to_host(out), _lib.to_host(protected)
     return out, protected
 
 
 def full_metrics(attn, cfg: MetricConfig, num_kv_heads: int) -> torch.Tensor:
     """Full-range metrics of an attention tensor: key j aggregates query rows
     i >= j + excluded (metrics.py:92-109).  No pooling, no protection."""
-    return _attn_call(attn, cfg, num_kv_heads, 1)
+    out = _attn_call(attn, cfg, num_kv_heads, 1)
+    return _lib.to_host(out) if _lib.is_host_array(attn) else out
 
 
 def prompt_metrics(attn, cfg: MetricConfig, num_kv_heads: int):
@@ -231,4 +235,6 @@ def prompt_metrics(attn, cfg: MetricConfig, num_kv_heads: int):
     if cfg.mode == WINDOW:
         return window_metrics(attn, cfg, num_kv_heads)
     m = full_metrics(attn, cfg, num_kv_heads)
+    if _lib.is_host_array(attn):
+        return m, np.zeros(m.shape[1], dtype=bool)
     return m, torch.zeros(m.shape[1], dtype=torch.bool, device=m.device)

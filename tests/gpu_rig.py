@@ -9,6 +9,12 @@ from oracle import kvc_oracle as O
 from paper_2410_00161_b200 import BlockManager, BlockTables, MetricsStore, UnifiedKVCache
 
 
+def as_np(x) -> np.ndarray:
+    """A facade result as NumPy: device tensors are copied back; the
+    reference-signature calls already return NumPy for NumPy inputs."""
+    return x.cpu().numpy() if torch.is_tensor(x) else np.asarray(x)
+
+
 class DevRig:
     def __init__(self, num_blocks, block_size, head_dim, layers, heads, max_seqs=8, max_blocks=None):
         self.cache = UnifiedKVCache(num_blocks, block_size, head_dim)

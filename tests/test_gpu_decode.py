@@ -13,7 +13,7 @@ import pytest
 import torch
 
 from golden_io import dec, load
-from gpu_rig import DevRig, bf16_round, random_state
+from gpu_rig import DevRig, as_np, bf16_round, random_state
 from oracle import kvc_oracle as O
 from oracle_rig import state_from_snapshot
 
@@ -92,11 +92,12 @@ def test_paged_attention_golden(i):
     rig.load(st)
     cfg = K.AttentionConfig(case["heads"] * case["r"], case["heads"], case["head_dim"], case["layers"])
     out, rows = K.paged_attention(q, rig.cache, rig.tables, case["seq"], case["layer"], cfg)
+    assert isinstance(out, np.ndarray) and all(isinstance(rw, np.ndarray) for rw in rows)  # NumPy in, NumPy out
     ref_out, ref_rows = O.paged_decode(st, q, case["seq"], case["layer"])
-    assert np.abs(out.cpu().numpy() - ref_out).max() < OUT_ATOL
+    assert np.abs(as_np(out) - ref_out).max() < OUT_ATOL
     for rw, rr in zip(rows, ref_rows):
         assert rw.shape == rr.shape
-        assert np.abs(rw.cpu().numpy() - rr).max() < ATOL
+        assert np.abs(as_np(rw) - rr).max() < ATOL
     mcfg = K.MetricConfig(mode="full", aggregation=case["aggregation"])
     K.accumulate_decode(rig.store, rig.tables, case["seq"], case["layer"], rows, mcfg)
     O.accumulate(st, case["seq"], case["layer"], ref_rows, case["aggregation"])

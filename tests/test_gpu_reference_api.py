@@ -16,6 +16,7 @@ import pytest
 import torch
 
 from golden_io import dec, load
+from gpu_rig import as_np
 
 pytestmark = pytest.mark.gpu
 
@@ -32,21 +33,25 @@ def test_attention_tensor_metrics_match_reference(i):
     q, k = dec(c["q"]), dec(c["k"])
     cfg = K.AttentionConfig(H * r, H, d, 1)
     out, attn = K.gqa_attention(q, k, np.zeros_like(k), cfg)
-    a = attn.cpu().numpy().astype(np.float64)
+    assert isinstance(attn, np.ndarray) and attn.dtype == np.float64  # NumPy in, NumPy out
+    a = as_np(attn)
     assert np.allclose(a.sum(axis=2), 1.0, atol=1e-5)
     assert np.all(np.triu(a, 1) == 0.0)
-    assert np.all(out.cpu().numpy() == 0.0)
+    assert np.all(as_np(out) == 0.0)
     wcfg = K.MetricConfig(mode="window", aggregation=c["aggregation"], window=c["window"], pool=c["pool"])
-    wm, prot = K.window_metrics(attn, wcfg, H)
-    want = dec(c["window_metrics"])
-    assert np.allclose(wm.cpu().numpy(), want, rtol=1e-4, atol=1e-6), np.abs(wm.cpu().numpy() - want).max()
-    assert np.array_equal(prot.cpu().numpy().astype(int), np.asarray(c["protected"]))
     fcfg = K.MetricConfig(mode="full", aggregation=c["aggregation"], excluded=c["excluded"])
-    fm = K.full_metrics(attn, fcfg, H)
-    want = dec(c["full_metrics"])
-    assert np.allclose(fm.cpu().numpy(), want, rtol=1e-4, atol=1e-6), np.abs(fm.cpu().numpy() - want).max()
-    pm, pp = K.prompt_metrics(attn, fcfg, H)
-    assert torch.equal(pm, fm) and not pp.any()
+    # once on the NumPy attention (NumPy results), once on a device tensor (device results)
+    for att in (attn, torch.as_tensor(attn, dtype=torch.float32, device="cuda")):
+        wm, prot = K.window_metrics(att, wcfg, H)
+        assert torch.is_tensor(wm) == torch.is_tensor(att)
+        want = dec(c["window_metrics"])
+        assert np.allclose(as_np(wm), want, rtol=1e-4, atol=1e-6), np.abs(as_np(wm) - want).max()
+        assert np.array_equal(as_np(prot).astype(int), np.asarray(c["protected"]))
+        fm = K.full_metrics(att, fcfg, H)
+        want = dec(c["full_metrics"])
+        assert np.allclose(as_np(fm), want, rtol=1e-4, atol=1e-6), np.abs(as_np(fm) - want).max()
+        pm, pp = K.prompt_metrics(att, fcfg, H)
+        assert np.array_equal(as_np(pm), as_np(fm)) and not as_np(pp).any()
 
 
 def test_gqa_attention_output_and_numeric_error():
@@ -55,9 +60,14 @@ def test_gqa_attention_output_and_numeric_error():
     q, k, v = (rng.standard_normal(s) for s in ((H * r, L, d), (H, L, d), (H, L, d)))
     out, attn = K.gqa_attention(q, k, v, K.AttentionConfig(H * r, H, d, 1))
     # out = attn @ v per group (float64 check of the fp32 kernel)
-    a = attn.cpu().numpy().astype(np.float64)
+    a = as_np(attn)
     want = np.concatenate([a[h * r:(h + 1) * r] @ v[h] for h in range(H)])
-    assert np.allclose(out.cpu().numpy(), want, atol=1e-5)
+    assert np.allclose(as_np(out), want, atol=1e-5)
+    # device tensors in: device tensors out, same values
+    dv = lambda x: torch.as_tensor(x, dtype=torch.float32, device="cuda")
+    out_d, attn_d = K.gqa_attention(dv(q), dv(k), dv(v), K.AttentionConfig(H * r, H, d, 1))
+    assert out_d.is_cuda and attn_d.is_cuda
+    assert np.array_equal(as_np(attn_d).astype(np.float64), a) and np.array_equal(as_np(out_d).astype(np.float64), as_np(out))
     q[1, 5, 0] = np.nan
     with pytest.raises(E.NumericError):
         K.gqa_attention(q, k, v, K.AttentionConfig(H * r, H, d, 1))
