@@ -61,7 +61,10 @@ void launch_pdl(void (*fn)(P...), dim3 grid, dim3 block, size_t smem, cudaStream
 constexpr int kBins = 2048;       // 11-bit digits
 constexpr int kThreads = 512;
 constexpr uint32_t kKeyInf = 0xFF800000u;  // f32_order_key(+inf)
-constexpr int kCand = 256;                 // candidate list capacity per head (short-head path)
+constexpr int kCand = 256;
+#ifndef KVC_SH_U
+#define KVC_SH_U 2  // short-head k_hist: uint4 key loads in flight per thread
+#endif                 // candidate list capacity per head (short-head path)
 
 struct EvictState {
   // per head (T = n_seqs * hp)
@@ -468,22 +471,35 @@ __device__ bool hist_body(const kvc_pool &p, const int32_t *rows, EvictState &S,
   // round's short heads (NT = 256) keep one, for occupancy
   constexpr int U = NT >= 512 ? 8 : 1;
   if constexpr (U == 1) {
-    for (int64_t base = 0; base < n; base += 4 * NT) {
-      const int64_t pos = base + 4 * threadIdx.x;  // max_slots is a multiple of 4
-      uint4 k4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-      if (pos < n) k4 = *reinterpret_cast<const uint4 *>(keys + pos);
-      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
-      uint32_t bin[4];
-      bool act[4];
+    // short heads (n <= 8192: 32-bit positions): KVC_SH_U uint4 loads per
+    // thread in flight (one kept the decode round's k_hist latency-bound:
+    // 4 dependent round trips per head at 2.2 TB/s)
+    constexpr int V = KVC_SH_U;
+    const int n32 = (int)n;
+    for (int base = 0; base < n32; base += 4 * NT * V) {
+      uint4 k4[V];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool in = pos + e < n;
-        const uint32_t top = kv[e] >> shift_hi;
-        below += (in && top < pre) ? 1 : 0;
-        bin[e] = (kv[e] >> shift) & dmask;
-        act[e] = in && top == pre;
+      for (int u = 0; u < V; ++u) {
+        const int pos = base + 4 * (u * NT + (int)threadIdx.x);  // max_slots is a multiple of 4
+        k4[u] = pos < n32 ? __ldcg(reinterpret_cast<const uint4 *>(keys + pos))
+                          : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
       }
-      hist_add4(hist, bin, act);
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int pos = base + 4 * (u * NT + (int)threadIdx.x);
+        const uint32_t kv[4] = {k4[u].x, k4[u].y, k4[u].z, k4[u].w};
+        uint32_t bin[4];
+        bool act[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool in = pos + e < n32;
+          const uint32_t top = kv[e] >> shift_hi;
+          below += (in && top < pre) ? 1 : 0;
+          bin[e] = (kv[e] >> shift) & dmask;
+          act[e] = in && top == pre;
+        }
+        hist_add4(hist, bin, act);
+      }
     }
   } else {
     for (int64_t base = 0; base < n; base += 4 * NT * U) {
