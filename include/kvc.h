@@ -208,7 +208,10 @@ typedef struct kvc_decode_args {
                                so this call's first work pull and its first KV
                                loads may run before that call finishes.  0 (the
                                safe default): everything waits for the prior
-                               stream work (allocator, compaction, scatter, ...). */
+                               stream work (allocator, compaction, scatter, ...).
+                               2: the first layer of such a chain - no early
+                               pull, but the launch leaves room on every SM for
+                               the next layer's early pull (d = 128). */
 } kvc_decode_args;
 
 int kvc_paged_decode(const kvc_pool *pool, const kvc_decode_args *args, void *stream);

@@ -50,7 +50,7 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
                  fresh: bool = True, out: torch.Tensor | None = None, out_f32: bool = False,
                  rows_out: torch.Tensor | None = None, rows_tensor: torch.Tensor | None = None,
                  host_rows: list | None = None, max_ctx: int | None = None,
-                 splits: int = 0, early_pull: bool = False) -> torch.Tensor:
+                 splits: int = 0, early_pull: int = 0) -> torch.Tensor:
     """Batched single-token decode for one layer (asynchronous, no host sync).
 
     query (B, n_q, d) bf16; k_new/v_new (B, H, d) bf16 are appended at each
@@ -63,7 +63,9 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     stream is this same call for another layer (consecutive layers of one
     decode step, with rows_tensor given so nothing is enqueued in between);
     the kernel may then start pulling work and streaming KV before that
-    launch finishes (kvc_decode_args.early_pull).
+    launch finishes (kvc_decode_args.early_pull).  2 marks the first layer
+    of such a chain: no early pull, but the launch leaves room for the next
+    layer's.
     """
     dev = cache.device
     B = query.shape[0]
@@ -96,7 +98,7 @@ def paged_decode(query: torch.Tensor, cache: UnifiedKVCache, tables: BlockTables
     a.append_fresh = int(fresh)
     a.max_ctx = max(1, int(max_ctx))
     a.splits = splits
-    a.early_pull = int(bool(early_pull))
+    a.early_pull = int(early_pull)  # False/0, True/1, or 2 (first layer of a chain)
     p = pool_struct(cache=cache, tables=tables, store=store)
     need = _lib.lib().kvc_decode_scratch_bytes(ctypes.byref(p), B, cfg.num_query_heads, a.max_ctx)
     with_scratch(p, dev, need)

@@ -76,6 +76,7 @@ struct Params {
   void *metric_stream;
   int counter_ready;
   int early_pull;   // kernel A pulls its first item before griddepcontrol.wait (host-checked)
+  int layer_chain;  // host only: a chain of consecutive layer launches (kvc_decode_args.early_pull 1 or 2)
   float *scores;    // [pairs][max_ctx_pad][r]
   float *part_ml;   // [pairs][n_ck][2][kHP]
   float *part_o;    // [pairs][n_ck][r][D]
@@ -863,11 +864,15 @@ int launch(Params &P, cudaStream_t s) {
   if (!pool_map(&tmK, P.p.k_cache, rows, D) || !pool_map(&tmV, P.p.v_cache, rows, D)) return KVC_ERR_CUDA;
   static const int env_stages = getenv("KVC_K1_STAGES") ? atoi(getenv("KVC_K1_STAGES")) : 0;  // experiments
   static const int env_ctas = getenv("KVC_K1_CTAS") ? atoi(getenv("KVC_K1_CTAS")) : 0;
-  // d = 128: a 2-stage ring (65 KB per CTA, 3 fit an SM) with the grid kept
-  // at 2 CTAs per SM, so the next layer's kernel A finds a free CTA slot on
-  // every SM and starts its early pull while this layer's CTAs drain
-  // (measured: B = 8 0.981 -> 0.972 ms/step, B = 64 5.921 -> 5.895)
-  P.stages = env_stages > 0 ? env_stages : (D >= 256 || D == 128) ? 2 : 3;
+  // d = 128 inside a chain of layer launches (the caller asked for the early
+  // pull, e.g. a DecodeStepGraph step): a 2-stage ring (65 KB per CTA, 3 fit
+  // an SM) with the grid kept at 2 CTAs per SM, so the next layer's kernel A
+  // finds a free CTA slot on every SM and starts its early pull while this
+  // layer's CTAs drain (graph step: B = 8 0.981 -> 0.972 ms, B = 64 5.921 ->
+  // 5.895).  Stand-alone launches keep the 3-stage ring on both slots
+  // (attention only at B = 8: 34.0 us per layer against 35.8 with 2 stages).
+  const bool spare_slot = D == 128 && P.layer_chain;
+  P.stages = env_stages > 0 ? env_stages : (D >= 256 || spare_slot) ? 2 : 3;
   const int smem = stream_smem(D, P.stages);
   auto fa = k_decode_stream<D>;
   auto fb = k_decode_finish<D>;
@@ -889,7 +894,7 @@ int launch(Params &P, cudaStream_t s) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fa, kThreads, smem);
   if (per_sm < 1) return KVC_ERR_UNSUPPORTED;
-  const int cap_sm = env_ctas > 0 ? env_ctas : D == 128 ? 2 : 0;
+  const int cap_sm = env_ctas > 0 ? env_ctas : spare_slot ? 2 : 0;
   if (cap_sm > 0 && cap_sm < per_sm) per_sm = cap_sm;
   int grid = n_sm * per_sm;
   if (grid > P.n_items) grid = P.n_items;
@@ -1058,12 +1063,14 @@ int kvc_decode_mma(const kvc_pool *pool, const kvc_decode_args *a, int, int, cud
     const long long n_prev = it == last.end() ? 0 : it->second.first;
     const int layer_prev = it == last.end() ? -1 : it->second.second;
     parity = (int)(n_prev & 1);
-    early = a->early_pull && a->queue && layer_prev >= 0 && layer_prev != a->layer && !getenv("KVC_NO_EARLY_PULL");
+    early = a->early_pull == 1 && a->queue && layer_prev >= 0 && layer_prev != a->layer &&
+            !getenv("KVC_NO_EARLY_PULL");
   }
   P.counter = qbase + parity;
   P.pair_done = qbase + 2;
   P.counter_ready = a->queue ? 1 : 0;
   P.early_pull = early ? 1 : 0;
+  P.layer_chain = a->early_pull == 1 || a->early_pull == 2;
   int64_t off = ((int64_t)(2 + a->batch * H) * 4 + 255) / 256 * 256;
   P.scores = reinterpret_cast<float *>(base + off);
   off += (int64_t)a->batch * H * P.max_ctx_pad * r * 4;

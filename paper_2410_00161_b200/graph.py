@@ -143,7 +143,8 @@ class DecodeStepGraph:
             a.metric_stream = self.side.cuda_stream if self.side is not None else None
             # layer m > 0 follows layer m-1's kernel B directly on the stream;
             # layer 0 follows the allocator, which writes tables / nblocks
-            a.early_pull = int(m > 0)
+            # (2: no early pull, but room for layer 1's)
+            a.early_pull = 1 if m > 0 else 2
             args.append(a)
         self._keep = (pools, args)
         self.graphs = {}
@@ -275,6 +276,6 @@ class DecodeStepGraph:
         for m in range(self.tables.num_layers):
             paged_decode(self.q[m], self.cache, self.tables, None, m, self.cfg, store=self.store,
                          metric_mode=self.metric_mode, k_new=self.k_new[m], v_new=self.v_new[m], fresh=self.fresh,
-                         out=self.out[m], rows_tensor=self.rows_t, host_rows=self.rows, early_pull=m > 0)
+                         out=self.out[m], rows_tensor=self.rows_t, host_rows=self.rows, early_pull=1 if m > 0 else 2)
         if self.clear_fresh:
             self.store.clear_fresh(self.tables, self.seq_ids)
