@@ -73,11 +73,14 @@ for grp in ("k1", "k2", "k34", "scatter"):
 L.append("")
 L += ["## Same-box comparator: FlashInfer paged decode on the same pool (`profiles/r2_flashinfer_compare.json`)", "",
       "| kernel | ms / layer | GB/s |", "|---|---|---|"]
+L[-2] = "| batch | kernel | ms / layer | GB/s |"
+L[-1] = "|---|---|---|---|"
 for run in fi["runs"]:
-    L.append(f"| ours (K1, attention only) | {run['ours']['ms_per_layer']:.4f} | {run['ours']['gbs']:.0f} |")
+    B = run["batch"]
+    L.append(f"| {B} | ours (K1, attention only, layers chained) | {run['ours']['ms_per_layer']:.4f} | {run['ours']['gbs']:.0f} |")
     f_ = run["flashinfer"]
     if "ms_per_layer" in f_:
-        L.append(f"| FlashInfer {f_['version']} {f_['api']} | {f_['ms_per_layer']:.4f} | {f_['gbs']:.0f} |")
+        L.append(f"| {B} | FlashInfer {f_['version']} {f_['api']} | {f_['ms_per_layer']:.4f} | {f_['gbs']:.0f} |")
 L += ["", "## Reference test suite through the import swap (`profiles/r2_reference_suite.json`)", "",
       f"{rs['totals']['passed']} passed, {rs['totals']['failed']} failed, {rs['totals']['error']} modules not "
       "collected (see INTEGRATION.md for the failure categories).", "",

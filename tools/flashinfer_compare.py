@@ -88,8 +88,10 @@ def main():
 
     def ours():
         for m in range(layers):
+            # consecutive layers on one stream, as a decode step issues them
+            # (layer m > 0 may pull work early; kvc_decode_args.early_pull)
             K.paged_decode(q[m], cache, tables, rows, m, cfg, metric_mode=0, out=outs[m], rows_tensor=rows_t,
-                           host_rows=[tables.row(s) for s in rows])
+                           host_rows=[tables.row(s) for s in rows], early_pull=1 if m > 0 else 2)
 
     t_ours = timeit(ours)
     res = {"what": __doc__.split("\n\n")[0].replace("\n", " "), "batch": B, "kv_heads": H, "group": r,
