@@ -317,3 +317,43 @@ def test_decode_step_raises_bound_once_per_step():
                            v_new=kv)
     assert rig.tables.ctx_bound[row] == before + 3
     assert int(rig.tables.ctx[row].max()) <= before + 3
+
+
+def test_layer_chain_equals_stand_alone_launches():
+    """A decode step's layers issued as a chain (kvc_decode_args.early_pull 2
+    for the first, 1 after: 2-stage ring, a spare CTA slot, early pulls) give
+    bit-identical outputs, K/V, tables and metrics to the same layers issued
+    stand-alone (early_pull 0: 3-stage ring, no early pull), at d = 128."""
+    rng = np.random.default_rng(128)
+    b, d, heads, r, layers = 16, 128, 8, 4, 4
+    seqs = list(range(16))
+    nblocks = int(len(seqs) * layers * heads * (900 // b + 2) * 1.6) + 64
+    st = random_state(rng, nblocks, b, d, layers, heads, seqs, 800, min_len=300)
+    cfg = K.AttentionConfig(heads * r, heads, d, layers)
+    qs = [bf16_round(rng.standard_normal((len(seqs), heads * r, d))) for _ in range(layers)]
+    kns = [bf16_round(rng.standard_normal((len(seqs), heads, d))) for _ in range(layers)]
+    vns = [bf16_round(rng.standard_normal((len(seqs), heads, d))) for _ in range(layers)]
+    results = []
+    for chain in (False, True):
+        rig = DevRig(nblocks, b, d, layers, heads, max_seqs=24, max_blocks=900 // b + 8)
+        rig.load(st)
+        rig.manager.allocate_decode_step(seqs)
+        dev = rig.cache.device
+        rows_t = torch.tensor([rig.tables.row(s) for s in seqs], dtype=torch.int32, device=dev)
+        host_rows = [rig.tables.row(s) for s in seqs]
+        outs = []
+        for layer in range(layers):
+            t = lambda x: torch.from_numpy(x).to(dev, torch.bfloat16)
+            outs.append(K.paged_decode(t(qs[layer]), rig.cache, rig.tables, seqs, layer, cfg, store=rig.store,
+                                       metric_mode=2, k_new=t(kns[layer]), v_new=t(vns[layer]), out_f32=True,
+                                       rows_tensor=rows_t, host_rows=host_rows,
+                                       early_pull=(1 if layer > 0 else 2) if chain else 0))
+        from paper_2410_00161_b200 import _lib
+        _lib.DeviceContext.get(dev).raise_status()
+        results.append(([o.cpu().numpy() for o in outs], rig.to_oracle()))
+    (o0, s0), (o1, s1) = results
+    for a, c in zip(o0, o1):
+        assert np.array_equal(a, c)
+    assert_same_ints(s0, s1)
+    assert np.array_equal(s0.metric, s1.metric)
+    assert np.array_equal(s0.keys, s1.keys) and np.array_equal(s0.values, s1.values)
