@@ -915,7 +915,7 @@ def main():
     if e2e:
         line["e2e"] = {"value": B * world * steps / (ms_e2e * 1e-3), "unit": UNIT,
                        "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU baseline is an N = 1 figure (rank 0)
         from threadpoolctl import threadpool_limits
 
         ctx = dec["ctx_before"].reshape(B, args.layers, args.kv_heads)
